@@ -1,0 +1,142 @@
+/*
+ * moe_b200.h - C ABI of the B200-native (sm_100a) MoE-layer forward path.
+ *
+ * Drop-in boundary for the reference package `moekit` (arXiv 2201.05596,
+ * /root/reference/pkg). The reference is pure Python/NumPy and has no FFI of
+ * its own: its boundary is the Python API of moekit.gating (gating.py:36-50)
+ * and the layer half of moekit.arch (arch.py:45-63). Each entry point below
+ * replaces the NumPy body of one of those functions (cited per function); the
+ * Python package paper_2201_05596_b200 binds them with ctypes and keeps the
+ * reference's names, argument meaning and exceptions.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers on the current CUDA device, allocated
+ *    by the caller (the library never allocates or frees). `stream` is a
+ *    cudaStream_t passed as void*; every call is stream-ordered and
+ *    asynchronous. The library holds no global mutable state besides cached
+ *    driver entry points, so calls are reentrant ("pure").
+ *  - Routing tables are int32 on device: ids/slots/local_rank are (S, k)
+ *    row-major, token-major flattening (gating.py:226). DROPPED slot = -1.
+ *  - Return value: 0 on success, MOE_EINVAL for bad arguments (checked before
+ *    any launch), MOE_ENODRV / MOE_ETMA for driver/tensor-map failures, or a
+ *    positive cudaError_t from the launch.
+ */
+#ifndef MOE_B200_H_
+#define MOE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_ABI_VERSION 1
+#define MOE_OK 0
+#define MOE_EINVAL (-22)
+#define MOE_ENODRV (-1001)
+#define MOE_ETMA (-1002)
+
+#define MOE_ROUTE_TILE 128 /* tokens per routing tile */
+
+enum { MOE_F32 = 0, MOE_BF16 = 1, MOE_F64 = 2 };
+enum { MOE_ACT_NONE = 0, MOE_ACT_GELU = 1 };
+
+int moe_abi_version(void);
+
+/* gating.top_k_gate (gating.py:142-163). logits (S, E) f32|f64; outputs
+ * ids (S, k) in descending-logit order with ties to the lower index,
+ * gate_probs (S, k) and optional probs (S, E) of the input dtype: the max-
+ * shifted softmax over all E, NOT renormalised over the k choices. */
+int moe_topk_gate(const void* logits, int dtype, int64_t S, int E, int k, int32_t* ids,
+                  void* gate_probs, void* probs, void* stream);
+
+/* gating.build_dispatch_plan (gating.py:211-247), split in three launches.
+ * T = ceil(S / MOE_ROUTE_TILE).
+ *  tiles: local_rank (S, k) = earlier same-expert assignments inside the
+ *         token's tile; tile_counts (T, E).
+ *  scan : tile_offsets (T, E) = rank_base[e] (nullable; the EP prefix over
+ *         lower ranks) + exclusive scan over tiles; totals (E) = this batch's
+ *         assignments per expert; kept (E) = how many of them fall below cap.
+ *  slots: slots (S, k) = tile_offsets + local_rank, or -1 at/over cap. */
+int moe_plan_tiles(const int32_t* ids, int64_t S, int E, int k, int32_t* local_rank,
+                   int32_t* tile_counts, void* stream);
+int moe_plan_scan(const int32_t* tile_counts, int64_t S, int E, int64_t cap,
+                  const int32_t* rank_base, int32_t* tile_offsets, int32_t* totals,
+                  int32_t* kept, void* stream);
+int moe_plan_slots(const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                   int64_t S, int E, int k, int64_t cap, int32_t* slots, void* stream);
+
+/* One-call plan: workspace = local_rank (S*k) | tile_counts (T*E) |
+ * tile_offsets (T*E) | totals (E), all int32. expert_load = kept. */
+size_t moe_plan_workspace_bytes(int64_t S, int E, int k);
+int moe_build_plan(const int32_t* ids, int64_t S, int E, int k, int64_t cap, int32_t* slots,
+                   int32_t* expert_load, void* ws, size_t ws_bytes, void* stream);
+
+/* gating.exclusive_scan_blelloch (gating.py:171-203). Integer input: exact
+ * int64 exclusive scan. Float input: the up-sweep/down-sweep over the zero-
+ * padded power-of-two buffer `tree` (m elements, in place), so results
+ * match the reference's float64 tree order bit for bit. */
+size_t moe_scan_workspace_bytes(int64_t n);
+int moe_exclusive_scan_i64(const int64_t* in, int64_t n, int64_t* out, void* ws, size_t ws_bytes,
+                           void* stream);
+int moe_blelloch_scan_f64(double* tree, int64_t m, void* stream);
+
+/* gating.scatter_tokens (gating.py:255-278): buf[(e*cap + slot)] = x[t] for
+ * kept assignments; rows are row_bytes wide (any dtype, exact copies).
+ * occupied (E*cap bytes, nullable) gets 1 at filled slots. The caller zero-
+ * fills buf/occupied first when it needs the reference's zero rows. */
+int moe_scatter(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                const int32_t* ids, const int32_t* slots, void* buf, uint8_t* occupied,
+                void* stream);
+
+/* Layer-path dispatch: plan_slots fused into scatter (slots written out). */
+int moe_dispatch(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                 const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                 int32_t* slots, void* buf, void* stream);
+
+/* gating.combine_tokens (gating.py:281-307) and the combine + residual of
+ * arch.forward_layer (arch.py:389-391, :395-413):
+ *   out[t] = ((x_resid[t]) + sum_j gate_prob[t,j] * y[row(t,j)]) + shared_out[t]
+ * row(t,j) = row_index[t,j] if row_index else ids*cap + slots (-1 = dropped).
+ * expert_order=1 sums contributions in ascending expert id (forward_layer),
+ * 0 in choice order (combine_tokens). dtype: F64 (gp F64, bit-exact adds),
+ * F32 (gp F32) or BF16 (gp F32, fp32 accumulation). */
+int moe_combine(const void* y, int dtype, int64_t S, int M, int E, int k, int64_t cap,
+                const int32_t* ids, const int32_t* slots, const int32_t* row_index,
+                const void* gate_probs, int gp_dtype, const void* x_resid, const void* shared_out,
+                void* out, int expert_order, void* stream);
+
+/* Gate GEMM (arch.py:384) fused with top_k_gate and plan_tiles on tcgen05:
+ * x bf16 (S, M); wg_t bf16 (Epad, M) = gate_w^T zero-padded to Epad rows,
+ * Epad = max(32, next_pow2(E)) <= 256. logits (S, E) f32 is optional. */
+int moe_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
+                       float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,
+                       int32_t* tile_counts, void* stream);
+
+/* Grouped expert GEMM on tcgen05 (the two halves of forward_ffn,
+ * arch.py:368-369): for each group g with rows[g] rows starting at row
+ * row_start[g] (or g*row_stride when row_start is NULL) of A (a_rows, K):
+ *   D[rows] = act(A[rows] @ B_w^T + bias_w),  w = weight_idx[g] (or g)
+ * A bf16 (a_rows, K); B bf16 (b_rows, K) with weight w at rows [w*N, w*N+N)
+ * (i.e. W^T, K-major); bias f32 (nweights, N) nullable; D bf16 (a_rows, N).
+ * rows == NULL means every group has rows_const rows. max_group_rows bounds
+ * rows[g] (sizes the launch). act: MOE_ACT_NONE | MOE_ACT_GELU (tanh form). */
+int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
+                          int N, const float* bias, void* D, int num_groups,
+                          const int32_t* row_start, int64_t row_stride, const int32_t* rows,
+                          int64_t rows_const, const int32_t* weight_idx, int64_t max_group_rows,
+                          int act, void* stream);
+
+/* fp32 SIMT variant (parity path). B f32 in the reference layout: weight w is
+ * (K, N) row-major at B + w*K*N. */
+int moe_grouped_gemm_f32(const float* A, int K, const float* B, int N, const float* bias, float* D,
+                         int num_groups, const int32_t* row_start, int64_t row_stride,
+                         const int32_t* rows, int64_t rows_const, const int32_t* weight_idx,
+                         int64_t max_group_rows, int act, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOE_B200_H_ */

@@ -1,0 +1,118 @@
+"""ctypes binding of libmoe_b200.so (the C ABI in include/moe_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no sm_100 GPU
+is present, every compute call raises. `load()` builds nothing; run
+`python -m paper_2201_05596_b200.build` (or __graft_entry__.build()) first.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmoe_b200.so")
+
+MOE_F32, MOE_BF16, MOE_F64 = 0, 1, 2
+MOE_ACT_NONE, MOE_ACT_GELU = 0, 1
+ROUTE_TILE = 128
+MOE_EINVAL = -22
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_int64
+_Z = ctypes.c_size_t
+
+# name -> (restype, argtypes), mirroring include/moe_b200.h
+SIGNATURES = {
+    "moe_abi_version": (_I, []),
+    "moe_topk_gate": (_I, [_P, _I, _L, _I, _I, _P, _P, _P, _P]),
+    "moe_plan_tiles": (_I, [_P, _L, _I, _I, _P, _P, _P]),
+    "moe_plan_scan": (_I, [_P, _L, _I, _L, _P, _P, _P, _P, _P]),
+    "moe_plan_slots": (_I, [_P, _P, _P, _L, _I, _I, _L, _P, _P]),
+    "moe_plan_workspace_bytes": (_Z, [_L, _I, _I]),
+    "moe_build_plan": (_I, [_P, _L, _I, _I, _L, _P, _P, _P, _Z, _P]),
+    "moe_scan_workspace_bytes": (_Z, [_L]),
+    "moe_exclusive_scan_i64": (_I, [_P, _L, _P, _P, _Z, _P]),
+    "moe_blelloch_scan_f64": (_I, [_P, _L, _P]),
+    "moe_scatter": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P]),
+    "moe_dispatch": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
+    "moe_combine": (_I, [_P, _I, _L, _I, _I, _I, _L, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P]),
+    "moe_gate_gemm_bf16": (_I, [_P, _P, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "moe_grouped_gemm_bf16": (_I, [_P, _L, _I, _P, _L, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L,
+                                   _I, _P]),
+    "moe_grouped_gemm_f32": (_I, [_P, _I, _P, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L, _I, _P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA extension (or an sm_100 device) is missing; no fallback exists."""
+
+
+def load():
+    """Load (once) and return the ctypes handle; raises NativeUnavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeUnavailable(
+                    f"{LIB_PATH} not built; run `python -m paper_2201_05596_b200.build`")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            if lib.moe_abi_version() != 1:
+                raise NativeUnavailable("libmoe_b200.so ABI version mismatch")
+            _lib = lib
+    return _lib
+
+
+def require_device(t: torch.Tensor | None = None) -> torch.device:
+    """The B200 path needs a CUDA sm_100 device; raise loudly otherwise."""
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: the B200 MoE path has no CPU fallback")
+    dev = t.device if (t is not None and t.is_cuda) else torch.device("cuda", torch.cuda.current_device())
+    major, _ = torch.cuda.get_device_capability(dev)
+    if major != 10:
+        raise NativeUnavailable(f"device {dev} is sm_{major}x; kernels are built for sm_100a")
+    load()
+    return dev
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def check(rc: int, what: str) -> None:
+    if rc == MOE_EINVAL:
+        raise ValueError(f"{what}: invalid arguments (MOE_EINVAL)")
+    if rc != 0:
+        raise RuntimeError(f"{what} failed with code {rc}")
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args), name)
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float32:
+        return MOE_F32
+    if dt == torch.bfloat16:
+        return MOE_BF16
+    if dt == torch.float64:
+        return MOE_F64
+    raise TypeError(f"unsupported dtype {dt}")

@@ -1,0 +1,401 @@
+"""MoE layer forward on the B200: drop-in for the layer half of ``moekit.arch``.
+
+Reference: arch.py:65-96 (FFN_MULT, LayerSpec), arch.py:316-413 (FfnParams,
+MoeLayerParams, init_layer_params, forward_ffn, forward_layer). Same names,
+fields, validation and exceptions. The forward is inference-only (no tape):
+the reference's tape-aware training use (arch.py:375-377) is out of scope.
+
+Two device paths, chosen by the activation dtype:
+
+* bf16 (the performance path): tcgen05 gate GEMM with the routing epilogue
+  -> capacity scan -> dispatch (slots fused) -> grouped tcgen05 GEMM1
+  (bias + tanh-GELU) -> grouped GEMM2 (bias) -> combine (+x, +shared MLP).
+* fp32 (the parity path for BASELINE config 1; NumPy inputs use it): the same
+  pipeline with an fp32 SIMT grouped GEMM and an accurate tanhf GELU.
+
+``MoeLayer`` holds the packed device weights (bf16 weights transposed to
+K-major for the tensor cores, fp32 biases) plus reusable workspaces; build it
+once and call it. ``forward_layer(x, spec, params)`` accepts either a
+``MoeLayer`` or reference-style ``MoeLayerParams`` (packed on every call).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .gating import GatingConfig
+from .tensor import ShapeError, Tensor, as_array
+
+__all__ = [
+    "ValidationError",
+    "FFN_MULT",
+    "LayerSpec",
+    "FfnParams",
+    "MoeLayerParams",
+    "init_layer_params",
+    "forward_ffn",
+    "forward_layer",
+    "MoeLayer",
+    "DenseFfn",
+]
+
+FFN_MULT = 4  # arch.py:65
+
+
+class ValidationError(ValueError):
+    """Structurally invalid layer description (arch.py:68)."""
+
+
+@dataclass(frozen=True)
+class LayerSpec:
+    """One transformer block's feed-forward slot (arch.py:72-96)."""
+
+    kind: str
+    hidden: int
+    experts: int = 0
+    residual: bool = False
+    gating: GatingConfig | None = None
+
+    def __post_init__(self) -> None:
+        if self.kind not in ("dense", "moe"):
+            raise ValidationError(f"unknown layer kind {self.kind!r}")
+        if self.hidden < 1:
+            raise ValidationError("hidden width must be positive")
+        if self.kind == "moe":
+            if self.experts < 1:
+                raise ValidationError("moe layer needs at least one expert")
+            if self.gating is None:
+                raise ValidationError("moe layer needs a gating config")
+            if self.gating.num_experts != self.experts:
+                raise ValidationError("gating config expert count mismatch")
+        else:
+            if self.experts != 0 or self.gating is not None or self.residual:
+                raise ValidationError("dense layer cannot carry expert fields")
+
+
+@dataclass
+class FfnParams:
+    """w1 (M, 4M), b1 (1, 4M), w2 (4M, M), b2 (1, M) (arch.py:321-329)."""
+
+    w1: object
+    b1: object
+    w2: object
+    b2: object
+
+    def leaves(self) -> list:
+        return [self.w1, self.b1, self.w2, self.b2]
+
+
+@dataclass
+class MoeLayerParams:
+    """gate_w (M, E), experts, optional shared MLP (arch.py:332-344)."""
+
+    gate_w: object
+    experts: tuple
+    shared: FfnParams | None = None
+
+    def leaves(self) -> list:
+        out = [self.gate_w]
+        for e in self.experts:
+            out.extend(e.leaves())
+        if self.shared is not None:
+            out.extend(self.shared.leaves())
+        return out
+
+
+def _init_ffn(m: int, rng: np.random.Generator, scale: float) -> FfnParams:
+    inner = FFN_MULT * m
+    return FfnParams(
+        w1=Tensor(rng.standard_normal((m, inner)) * scale),
+        b1=Tensor(np.zeros((1, inner))),
+        w2=Tensor(rng.standard_normal((inner, m)) * scale),
+        b2=Tensor(np.zeros((1, m))),
+    )
+
+
+def init_layer_params(spec: LayerSpec, rng: np.random.Generator, scale: float = 0.1):
+    """Host parameters with the reference's draw order (arch.py:347-365), so a
+    seeded rng gives the same weights as ``moekit.arch.init_layer_params``."""
+    if spec.kind == "dense":
+        return _init_ffn(spec.hidden, rng, scale)
+    return MoeLayerParams(
+        gate_w=Tensor(rng.standard_normal((spec.hidden, spec.experts)) * scale),
+        experts=tuple(_init_ffn(spec.hidden, rng, scale) for _ in range(spec.experts)),
+        shared=_init_ffn(spec.hidden, rng, scale) if spec.residual else None,
+    )
+
+
+# ---------------------------------------------------------------------------
+# packing
+# ---------------------------------------------------------------------------
+
+
+def _t(x, dev, dtype) -> torch.Tensor:
+    x = as_array(x)
+    if isinstance(x, torch.Tensor):
+        return x.to(device=dev, dtype=dtype)
+    return torch.as_tensor(np.asarray(x), device=dev).to(dtype)
+
+
+def _check_dtype(dtype: torch.dtype) -> torch.dtype:
+    if dtype not in (torch.bfloat16, torch.float32):
+        raise TypeError(f"layer dtype must be torch.bfloat16 or torch.float32, got {dtype}")
+    return dtype
+
+
+class DenseFfn:
+    """One packed FFN (the shared Residual-MoE MLP or a dense layer) on device."""
+
+    def __init__(self, p: FfnParams, hidden: int, dtype: torch.dtype, dev) -> None:
+        self.dtype, self.M, self.F = dtype, hidden, FFN_MULT * hidden
+        w1, w2 = _t(p.w1, dev, torch.float32), _t(p.w2, dev, torch.float32)
+        if tuple(w1.shape) != (self.M, self.F) or tuple(w2.shape) != (self.F, self.M):
+            raise ShapeError(f"ffn weights {tuple(w1.shape)}/{tuple(w2.shape)} do not match "
+                             f"hidden {hidden}")
+        self.b1 = _t(p.b1, dev, torch.float32).reshape(1, self.F).contiguous()
+        self.b2 = _t(p.b2, dev, torch.float32).reshape(1, self.M).contiguous()
+        if dtype == torch.bfloat16:  # W^T, K-major for tcgen05
+            self.w1 = w1.t().contiguous().to(dtype)
+            self.w2 = w2.t().contiguous().to(dtype)
+        else:
+            self.w1, self.w2 = w1.contiguous(), w2.contiguous()
+
+    def __call__(self, x: torch.Tensor, h: torch.Tensor | None = None,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+        s = x.shape[0]
+        h = torch.empty((s, self.F), dtype=self.dtype, device=x.device) if h is None else h
+        out = torch.empty((s, self.M), dtype=self.dtype, device=x.device) if out is None else out
+        _grouped_gemm(self.dtype, x, s, self.M, self.w1, self.F, self.b1, h, 1, None, 0, None, s,
+                      s, _lib.MOE_ACT_GELU)
+        _grouped_gemm(self.dtype, h, s, self.F, self.w2, self.M, self.b2, out, 1, None, 0, None, s,
+                      s, _lib.MOE_ACT_NONE)
+        return out
+
+
+def _grouped_gemm(dtype, a, a_rows, K, w, N, bias, d, G, row_start, row_stride, rows, rows_const,
+                  max_rows, act):
+    st = _lib.stream_ptr()
+    if dtype == torch.bfloat16:
+        _lib.call("moe_grouped_gemm_bf16", a.data_ptr(), a_rows, K, w.data_ptr(),
+                  w.numel() // K, N, _lib.ptr(bias), d.data_ptr(), G, _lib.ptr(row_start),
+                  row_stride, _lib.ptr(rows), rows_const, None, max_rows, act, st)
+    else:
+        _lib.call("moe_grouped_gemm_f32", a.data_ptr(), K, w.data_ptr(), N, _lib.ptr(bias),
+                  d.data_ptr(), G, _lib.ptr(row_start), row_stride, _lib.ptr(rows), rows_const,
+                  None, max_rows, act, st)
+
+
+class MoeLayer:
+    """A Standard / Residual (PR-MoE) MoE layer packed for the B200.
+
+    Device layout (HBM): gate weight (bf16: W_g^T zero-padded to Epad rows;
+    fp32: W_g as (M, E)); expert weights stacked per expert (bf16: W1^T as
+    (E*F, M) and W2^T as (E*M, F), K-major; fp32: (E, M, F) and (E, F, M));
+    biases fp32 (E, F) / (E, M). Activations (S, M) row-major.
+    """
+
+    def __init__(self, spec: LayerSpec, params: MoeLayerParams, dtype=torch.bfloat16,
+                 device=None) -> None:
+        if spec.kind != "moe":
+            raise ValidationError("MoeLayer needs a moe LayerSpec")
+        dev = _lib.require_device(None) if device is None else torch.device(device)
+        _lib.load()
+        self.spec, self.dtype, self.device = spec, _check_dtype(dtype), dev
+        M, E = spec.hidden, spec.experts
+        F = FFN_MULT * M
+        self.M, self.E, self.F, self.k = M, E, F, spec.gating.k
+        if len(params.experts) != E:
+            raise ShapeError(f"{len(params.experts)} experts given, spec has {E}")
+        gw = _t(params.gate_w, dev, torch.float32)
+        if tuple(gw.shape) != (M, E):
+            raise ShapeError(f"gate_w shape {tuple(gw.shape)} != ({M}, {E})")
+        w1 = torch.stack([_t(p.w1, dev, torch.float32) for p in params.experts])
+        w2 = torch.stack([_t(p.w2, dev, torch.float32) for p in params.experts])
+        if tuple(w1.shape) != (E, M, F) or tuple(w2.shape) != (E, F, M):
+            raise ShapeError("expert weight shapes do not match the spec")
+        self.b1 = torch.stack([_t(p.b1, dev, torch.float32).reshape(F) for p in params.experts])
+        self.b2 = torch.stack([_t(p.b2, dev, torch.float32).reshape(M) for p in params.experts])
+        if self.dtype == torch.bfloat16:
+            if E > 256:
+                raise ValueError("the bf16 tcgen05 gate supports E <= 256")
+            if M % 8:
+                raise ValueError("the bf16 tensor-core path needs hidden % 8 == 0")
+            self.epad = max(32, 1 << (E - 1).bit_length())
+            wg_t = torch.zeros((self.epad, M), dtype=torch.bfloat16, device=dev)
+            wg_t[:E] = gw.t().to(torch.bfloat16)
+            self.wg = wg_t
+            self.w1 = w1.transpose(1, 2).reshape(E * F, M).contiguous().to(torch.bfloat16)
+            self.w2 = w2.transpose(1, 2).reshape(E * M, F).contiguous().to(torch.bfloat16)
+        else:
+            self.wg = gw.contiguous()
+            self.w1, self.w2 = w1.contiguous(), w2.contiguous()
+        del w1, w2
+        self.shared = (DenseFfn(params.shared, M, self.dtype, dev)
+                       if (spec.residual and params.shared is not None) else None)
+        if spec.residual and params.shared is None:
+            raise ValidationError("residual layer needs shared MLP params")
+        self._ws: dict = {}
+
+    # -- workspace -----------------------------------------------------------
+    def workspace(self, S: int) -> dict:
+        ws = self._ws.get(S)
+        if ws is not None:
+            return ws
+        self._ws.clear()
+        dev, dt, E, M, F, k = self.device, self.dtype, self.E, self.M, self.F, self.k
+        cap = self.spec.gating.capacity(S)
+        T = (S + _lib.ROUTE_TILE - 1) // _lib.ROUTE_TILE
+        i32 = dict(dtype=torch.int32, device=dev)
+        ws = dict(
+            cap=cap, T=T,
+            ids=torch.empty((S, k), **i32), slots=torch.empty((S, k), **i32),
+            local_rank=torch.empty((S, k), **i32),
+            gp=torch.empty((S, k), dtype=torch.float32, device=dev),
+            tile_counts=torch.empty((max(T, 1), E), **i32),
+            tile_offsets=torch.empty((max(T, 1), E), **i32),
+            totals=torch.empty(E, **i32), load=torch.empty(E, **i32),
+            xbuf=torch.empty((max(E * cap, 1), M), dtype=dt, device=dev),
+            h=torch.empty((max(E * cap, 1), F), dtype=dt, device=dev),
+            y=torch.empty((max(E * cap, 1), M), dtype=dt, device=dev),
+        )
+        if dt == torch.float32:
+            ws["logits"] = torch.empty((S, E), dtype=torch.float32, device=dev)
+        if self.shared is not None:
+            ws["hs"] = torch.empty((S, F), dtype=dt, device=dev)
+            ws["ys"] = torch.empty((S, M), dtype=dt, device=dev)
+        self._ws[S] = ws
+        return ws
+
+    # -- forward ---------------------------------------------------------------
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None,
+                 logits_out: torch.Tensor | None = None) -> torch.Tensor:
+        return self.forward(x, out, logits_out)
+
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None,
+                logits_out: torch.Tensor | None = None) -> torch.Tensor:
+        """out = x + combine(experts(dispatch(x))) [+ shared MLP(x)]
+        (arch.py:372-392). ``logits_out`` (S, E) fp32 receives the gate logits
+        the routing decided on (the parity tests feed them to the oracle)."""
+        if x.dim() != 2 or x.shape[1] != self.M:
+            raise ShapeError(f"batch width {tuple(x.shape)} does not match layer hidden {self.M}")
+        if x.dtype != self.dtype or x.device != self.device:
+            x = x.to(device=self.device, dtype=self.dtype)
+        x = x.contiguous()
+        S = x.shape[0]
+        out = torch.empty_like(x) if out is None else out
+        if S == 0:
+            return out
+        ws = self.workspace(S)
+        cap, E, M, F, k = ws["cap"], self.E, self.M, self.F, self.k
+        st = _lib.stream_ptr()
+        ids, gp, lr, tc = ws["ids"], ws["gp"], ws["local_rank"], ws["tile_counts"]
+        if self.dtype == torch.bfloat16:
+            _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k,
+                      _lib.ptr(logits_out), ids.data_ptr(), gp.data_ptr(), lr.data_ptr(),
+                      tc.data_ptr(), st)
+        else:
+            logits = ws["logits"] if logits_out is None else logits_out
+            _grouped_gemm(self.dtype, x, S, M, self.wg, E, None, logits, 1, None, 0, None, S, S,
+                          _lib.MOE_ACT_NONE)
+            _lib.call("moe_topk_gate", logits.data_ptr(), _lib.MOE_F32, S, E, k, ids.data_ptr(),
+                      gp.data_ptr(), None, st)
+            _lib.call("moe_plan_tiles", ids.data_ptr(), S, E, k, lr.data_ptr(), tc.data_ptr(), st)
+        _lib.call("moe_plan_scan", tc.data_ptr(), S, E, cap, None, ws["tile_offsets"].data_ptr(),
+                  ws["totals"].data_ptr(), ws["load"].data_ptr(), st)
+        _lib.call("moe_dispatch", x.data_ptr(), S, M * x.element_size(), E, k, cap, ids.data_ptr(),
+                  lr.data_ptr(), ws["tile_offsets"].data_ptr(), ws["slots"].data_ptr(),
+                  ws["xbuf"].data_ptr(), st)
+        if cap > 0:
+            _grouped_gemm(self.dtype, ws["xbuf"], E * cap, M, self.w1, F, self.b1, ws["h"], E,
+                          None, cap, ws["load"], 0, cap, _lib.MOE_ACT_GELU)
+            _grouped_gemm(self.dtype, ws["h"], E * cap, F, self.w2, M, self.b2, ws["y"], E, None,
+                          cap, ws["load"], 0, cap, _lib.MOE_ACT_NONE)
+        shared_out = None
+        if self.shared is not None:
+            shared_out = self.shared(x, ws["hs"], ws["ys"])
+        gp_code = _lib.MOE_F32
+        _lib.call("moe_combine", ws["y"].data_ptr(), _lib.dtype_code(self.dtype), S, M, E, k, cap,
+                  ids.data_ptr(), ws["slots"].data_ptr(), None, gp.data_ptr(), gp_code,
+                  x.data_ptr(), _lib.ptr(shared_out), out.data_ptr(), 1, st)
+        return out
+
+    def plan(self, S: int):
+        """(ids, gate_probs, slots, expert_load, capacity) of the last forward of size S."""
+        ws = self._ws[S]
+        return ws["ids"], ws["gp"], ws["slots"], ws["load"], ws["cap"]
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped entry points
+# ---------------------------------------------------------------------------
+
+
+def _input(x):
+    """-> (device tensor, how to return). NumPy/Tensor inputs run the fp32 path."""
+    raw = as_array(x)
+    if isinstance(raw, torch.Tensor):
+        dev = _lib.require_device(raw)
+        t = raw.to(dev)
+        if t.dtype not in (torch.bfloat16, torch.float32):
+            t = t.float()
+        return t, "torch"
+    arr = np.asarray(raw, dtype=np.float64)
+    if arr.ndim != 2:
+        raise ShapeError(f"batch must be 2-D, got shape {arr.shape}")
+    dev = _lib.require_device(None)
+    kind = "tensor" if hasattr(x, "value") else "numpy"
+    return torch.as_tensor(arr, device=dev).float(), kind
+
+
+def _output(t: torch.Tensor, kind: str):
+    if kind == "torch":
+        return t
+    arr = t.detach().float().cpu().numpy().astype(np.float64)
+    return Tensor(arr) if kind == "tensor" else arr
+
+
+def forward_ffn(x, p: FfnParams):
+    """gelu(x @ w1 + b1) @ w2 + b2 (arch.py:368-369) on the device."""
+    t, kind = _input(x)
+    m = t.shape[1]
+    if isinstance(p, DenseFfn):
+        ffn = p
+    else:
+        w1 = as_array(p.w1)
+        ffn = DenseFfn(p, int(w1.shape[0]), t.dtype, t.device)
+    if m != ffn.M:
+        raise ShapeError(f"batch width {m} does not match ffn width {ffn.M}")
+    return _output(ffn(t.to(ffn.dtype).contiguous()), kind)
+
+
+def forward_layer(x, spec: LayerSpec, params):
+    """One block's feed-forward slot with its residual skip (arch.py:372-392).
+
+    ``params``: a ``MoeLayer`` (pre-packed, the fast path), reference-style
+    ``MoeLayerParams`` for a moe spec, or ``FfnParams`` for a dense spec.
+    NumPy / Tensor inputs run the fp32 path and come back as float64."""
+    t, kind = _input(x)
+    if t.shape[1] != spec.hidden:
+        raise ShapeError(f"batch width {t.shape[1]} does not match layer hidden {spec.hidden}")
+    if spec.kind == "dense":
+        ffn = params if isinstance(params, DenseFfn) else DenseFfn(params, spec.hidden, t.dtype,
+                                                                  t.device)
+        xt = t.to(ffn.dtype).contiguous()
+        y = ffn(xt)
+        out = torch.empty_like(xt)
+        s = xt.shape[0]
+        if s:
+            # out = x + ffn(x): the combine kernel with no routed rows (k=1, all dropped)
+            ids = torch.zeros((s, 1), dtype=torch.int32, device=t.device)
+            slots = torch.full((s, 1), -1, dtype=torch.int32, device=t.device)
+            gp = torch.zeros((s, 1), dtype=torch.float32, device=t.device)
+            _lib.call("moe_combine", None, _lib.dtype_code(xt.dtype), s, spec.hidden, 1, 1, 0,
+                      ids.data_ptr(), slots.data_ptr(), None, gp.data_ptr(), _lib.MOE_F32,
+                      xt.data_ptr(), y.data_ptr(), out.data_ptr(), 1, _lib.stream_ptr())
+        return _output(out, kind)
+    layer = params if isinstance(params, MoeLayer) else MoeLayer(spec, params, t.dtype, t.device)
+    return _output(layer(t), kind)

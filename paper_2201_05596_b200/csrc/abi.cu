@@ -1,0 +1,166 @@
+// extern "C" entry points of libmoe_b200.so (declared in include/moe_b200.h).
+// Arguments are validated here, before any launch, so a bad call returns
+// MOE_EINVAL instead of faulting the device.
+#include "moe_kernels.h"
+
+#define CHECK(cond)            \
+  do {                         \
+    if (!(cond)) return MOE_EINVAL; \
+  } while (0)
+
+static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline int64_t tiles_of(int64_t S) { return (S + MOE_ROUTE_TILE - 1) / MOE_ROUTE_TILE; }
+
+extern "C" {
+
+int moe_abi_version(void) { return MOE_ABI_VERSION; }
+
+int moe_topk_gate(const void* logits, int dtype, int64_t S, int E, int k, int32_t* ids,
+                  void* gate_probs, void* probs, void* stream) {
+  CHECK(S >= 0 && E >= 1 && (k == 1 || k == 2) && k <= E);
+  CHECK(dtype == MOE_F32 || dtype == MOE_F64);
+  if (S == 0) return MOE_OK;
+  CHECK(logits && ids && gate_probs);
+  return moe::launch_topk_gate(logits, dtype, S, E, k, ids, gate_probs, probs, S_(stream));
+}
+
+int moe_plan_tiles(const int32_t* ids, int64_t S, int E, int k, int32_t* local_rank,
+                   int32_t* tile_counts, void* stream) {
+  CHECK(S >= 0 && E >= 1 && E <= 3072 && (k == 1 || k == 2));
+  if (S == 0) return MOE_OK;
+  CHECK(ids && local_rank && tile_counts);
+  return moe::launch_plan(ids, S, k, E, 0, nullptr, local_rank, tile_counts, nullptr, nullptr,
+                          nullptr, nullptr, true, false, false, S_(stream));
+}
+
+int moe_plan_scan(const int32_t* tile_counts, int64_t S, int E, int64_t cap,
+                  const int32_t* rank_base, int32_t* tile_offsets, int32_t* totals, int32_t* kept,
+                  void* stream) {
+  CHECK(S >= 0 && E >= 1 && cap >= 0);
+  CHECK(totals && kept && (S == 0 || (tile_counts && tile_offsets)));
+  return moe::launch_plan(nullptr, S, 1, E, cap, rank_base, nullptr,
+                          const_cast<int32_t*>(tile_counts), tile_offsets, totals, kept, nullptr,
+                          false, true, false, S_(stream));
+}
+
+int moe_plan_slots(const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                   int64_t S, int E, int k, int64_t cap, int32_t* slots, void* stream) {
+  CHECK(S >= 0 && E >= 1 && (k == 1 || k == 2) && cap >= 0);
+  if (S == 0) return MOE_OK;
+  CHECK(ids && local_rank && tile_offsets && slots);
+  return moe::launch_plan(ids, S, k, E, cap, nullptr, const_cast<int32_t*>(local_rank), nullptr,
+                          const_cast<int32_t*>(tile_offsets), nullptr, nullptr, slots, false,
+                          false, true, S_(stream));
+}
+
+size_t moe_plan_workspace_bytes(int64_t S, int E, int k) {
+  if (S < 0 || E < 1 || k < 1) return 0;
+  const int64_t T = tiles_of(S);
+  return (size_t)(S * k + 2 * T * E + E) * sizeof(int32_t);
+}
+
+int moe_build_plan(const int32_t* ids, int64_t S, int E, int k, int64_t cap, int32_t* slots,
+                   int32_t* expert_load, void* ws, size_t ws_bytes, void* stream) {
+  CHECK(S >= 0 && E >= 1 && E <= 3072 && (k == 1 || k == 2) && cap >= 0 && expert_load);
+  CHECK(ws_bytes >= moe_plan_workspace_bytes(S, E, k) && ws);
+  const int64_t T = tiles_of(S);
+  int32_t* w = static_cast<int32_t*>(ws);
+  int32_t* local_rank = w;
+  int32_t* tile_counts = local_rank + S * k;
+  int32_t* tile_offsets = tile_counts + T * E;
+  int32_t* totals = tile_offsets + T * E;
+  if (S > 0) CHECK(ids && slots);
+  return moe::launch_plan(ids, S, k, E, cap, nullptr, local_rank, tile_counts, tile_offsets, totals,
+                          expert_load, slots, S > 0, true, S > 0, S_(stream));
+}
+
+size_t moe_scan_workspace_bytes(int64_t n) {
+  if (n < 0) return 0;
+  return (size_t)moe::scan_i64_workspace_elems(n) * sizeof(int64_t);
+}
+
+int moe_exclusive_scan_i64(const int64_t* in, int64_t n, int64_t* out, void* ws, size_t ws_bytes,
+                           void* stream) {
+  CHECK(n >= 0);
+  if (n == 0) return MOE_OK;
+  CHECK(in && out && ws && ws_bytes >= moe_scan_workspace_bytes(n));
+  return moe::launch_scan_i64(in, n, out, static_cast<int64_t*>(ws), S_(stream));
+}
+
+int moe_blelloch_scan_f64(double* tree, int64_t m, void* stream) {
+  CHECK(m >= 1 && (m & (m - 1)) == 0 && tree);
+  return moe::launch_blelloch_f64(tree, m, S_(stream));
+}
+
+int moe_scatter(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                const int32_t* ids, const int32_t* slots, void* buf, uint8_t* occupied,
+                void* stream) {
+  CHECK(S >= 0 && row_bytes >= 0 && E >= 1 && (k == 1 || k == 2) && cap >= 0);
+  CHECK(row_bytes % 2 == 0);
+  if (S == 0 || cap == 0) return MOE_OK;
+  CHECK(x && ids && slots && buf);
+  return moe::launch_scatter(x, S, row_bytes, k, E, cap, ids, const_cast<int32_t*>(slots), nullptr,
+                             nullptr, buf, occupied, S_(stream));
+}
+
+int moe_dispatch(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                 const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                 int32_t* slots, void* buf, void* stream) {
+  CHECK(S >= 0 && row_bytes >= 0 && row_bytes % 2 == 0 && E >= 1 && (k == 1 || k == 2) &&
+        cap >= 0);
+  if (S == 0) return MOE_OK;
+  CHECK(x && ids && local_rank && tile_offsets && slots && (buf || cap == 0));
+  return moe::launch_scatter(x, S, row_bytes, k, E, cap, ids, slots, local_rank, tile_offsets, buf,
+                             nullptr, S_(stream));
+}
+
+int moe_combine(const void* y, int dtype, int64_t S, int M, int E, int k, int64_t cap,
+                const int32_t* ids, const int32_t* slots, const int32_t* row_index,
+                const void* gate_probs, int gp_dtype, const void* x_resid, const void* shared_out,
+                void* out, int expert_order, void* stream) {
+  CHECK(S >= 0 && M >= 0 && E >= 1 && (k == 1 || k == 2) && cap >= 0);
+  if (S == 0 || M == 0) return MOE_OK;
+  CHECK(ids && gate_probs && out && (row_index || slots));
+  CHECK(y || cap == 0 || row_index);
+  return moe::launch_combine(y, dtype, S, M, k, E, cap, ids, slots, row_index, gate_probs, gp_dtype,
+                             x_resid, shared_out, out, expert_order, S_(stream));
+}
+
+int moe_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
+                       float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,
+                       int32_t* tile_counts, void* stream) {
+  CHECK(S >= 0 && M >= 8 && M % 8 == 0 && E >= 1 && E <= 256 && (k == 1 || k == 2) && k <= E);
+  if (S == 0) return MOE_OK;
+  CHECK(x && wg_t && ids && gate_probs && local_rank && tile_counts);
+  return moe::launch_gate_gemm_bf16(x, wg_t, S, M, E, k, logits, ids, gate_probs, local_rank,
+                                    tile_counts, S_(stream));
+}
+
+int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
+                          int N, const float* bias, void* D, int num_groups,
+                          const int32_t* row_start, int64_t row_stride, const int32_t* rows,
+                          int64_t rows_const, const int32_t* weight_idx, int64_t max_group_rows,
+                          int act, void* stream) {
+  CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1);
+  CHECK(act == MOE_ACT_NONE || act == MOE_ACT_GELU);
+  CHECK(max_group_rows >= 0 && rows_const >= 0);
+  if (a_rows == 0 || max_group_rows == 0) return MOE_OK;
+  CHECK(A && B && D);
+  return moe::launch_grouped_gemm_bf16(A, a_rows, K, B, b_rows, N, bias, D, num_groups, row_start,
+                                       row_stride, rows, rows_const, weight_idx, max_group_rows,
+                                       act, S_(stream));
+}
+
+int moe_grouped_gemm_f32(const float* A, int K, const float* B, int N, const float* bias, float* D,
+                         int num_groups, const int32_t* row_start, int64_t row_stride,
+                         const int32_t* rows, int64_t rows_const, const int32_t* weight_idx,
+                         int64_t max_group_rows, int act, void* stream) {
+  CHECK(K >= 1 && N >= 1 && num_groups >= 1 && max_group_rows >= 0);
+  CHECK(act == MOE_ACT_NONE || act == MOE_ACT_GELU);
+  if (max_group_rows == 0) return MOE_OK;
+  CHECK(A && B && D);
+  return moe::launch_grouped_gemm_f32(A, K, B, N, bias, D, num_groups, row_start, row_stride, rows,
+                                      rows_const, weight_idx, max_group_rows, act, S_(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,522 @@
+// tcgen05 + TMA grouped GEMM for sm_100a (bf16 in, fp32 accumulate in TMEM).
+//
+//   D[rows of group g] = epilogue( A[rows of g] (r x K) . B_w(g)^T (K x N) )
+//
+// Used for
+//   * the expert FFN halves of forward_ffn (arch.py:368-369): GEMM1 with a
+//     bias + tanh-GELU epilogue, GEMM2 with a bias epilogue, one group per
+//     expert (or per (source rank, expert) segment under expert parallelism);
+//   * the gate GEMM (arch.py:384) with a fused routing epilogue: softmax over
+//     all E logits, top-k with lower-index ties (gating.py:142-163) and the
+//     per-tile capacity ranks that build_dispatch_plan scans (gating.py:211-247).
+//
+// Persistent kernel, one CTA per SM, 6 warps:
+//   warp 0    TMA producer (A and B tiles, 128B swizzle, STAGES-deep ring)
+//   warp 1    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5 epilogue: tcgen05.ld (32 lanes x 32 columns) -> registers -> HBM
+// The fp32 accumulator is double buffered in TMEM (2 x BN columns) so the
+// epilogue of tile i overlaps the MMAs of tile i+1.
+#include "common.cuh"
+#include "moe_kernels.h"
+
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+namespace moe {
+
+enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2 };
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int kThreads = 192;
+constexpr int kMaxGroups = 2048;
+
+struct GemmArgs {
+  const float* bias;          // [num_weights, N] fp32 (may be null)
+  __nv_bfloat16* D;           // [a_rows, N]
+  int K, N;
+  int G;                      // groups
+  const int32_t* row_start;   // [G] or null -> g * row_stride
+  int64_t row_stride;
+  const int32_t* rows;        // [G] device rows per group (or null -> rows_const)
+  int64_t rows_const;
+  const int32_t* weight_idx;  // [G] or null -> g
+  // gate epilogue
+  int E, k;
+  int64_t S;
+  float* logits;              // [S, E] optional
+  int32_t* ids;               // [S, k]
+  float* gate_probs;          // [S, k]
+  int32_t* local_rank;        // [S, k]
+  int32_t* tile_counts;       // [T, E]
+};
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOff = STAGES * kStageBytes;
+  static constexpr int kBarBytes = (2 * STAGES + 4) * 8 + 16;
+  static constexpr int kTileOff = kBarOff + kBarBytes;
+  static constexpr int kTotal = kTileOff + (kMaxGroups + 1) * 4 + 1024;  // +1024 align slack
+};
+
+template <int BN>
+constexpr uint32_t tmem_cols() {
+  return (2 * BN) < 32 ? 32 : (2 * BN);
+}
+
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
+  using L = Smem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* tile_start = reinterpret_cast<int32_t*>(smem + L::kTileOff);
+
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+  const int G = args.G;
+  const int n_blocks = (args.N + BN - 1) / BN;
+
+  // ---- per-CTA tile table: tile_start[g] = sum_{g'<g} ceil(rows/BM) * n_blocks
+  if (warp == 0) {
+    const int per = (G + 31) / 32;
+    const int g0 = lane * per;
+    int local = 0;
+    for (int g = g0; g < min(G, g0 + per); ++g) {
+      const int64_t r = args.rows ? args.rows[g] : args.rows_const;
+      local += (int)((r + BM - 1) / BM) * n_blocks;
+    }
+    int incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
+    }
+    int run = incl - local;
+    for (int g = g0; g < min(G, g0 + per); ++g) {
+      tile_start[g] = run;
+      const int64_t r = args.rows ? args.rows[g] : args.rows_const;
+      run += (int)((r + BM - 1) / BM) * n_blocks;
+    }
+    if (lane == 31) tile_start[G] = incl;
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&tfull[a], 1);
+        mbar_init(&tempty[a], 4);
+      }
+      mbar_fence_init();
+    }
+    __syncwarp();
+    tmem_alloc(tmem_slot, tmem_cols<BN>());
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = tile_start[G];
+
+  // tile -> (group, m block, n block); n-major within a group so CTAs that run
+  // concurrently share the B (weight) tile through L2.
+  auto decode = [&](int tile, int& g, int& mb, int& nb) {
+    while (tile_start[g + 1] <= tile) ++g;
+    const int local = tile - tile_start[g];
+    const int64_t r = args.rows ? args.rows[g] : args.rows_const;
+    const int mblocks = (int)((r + BM - 1) / BM);
+    nb = local / mblocks;
+    mb = local - nb * mblocks;
+  };
+
+  if (warp == 0) {
+    // ===================== TMA producer
+    int stage = 0;
+    uint32_t phase = 0;
+    int g = 0;
+    const int num_kb = (args.K + BK - 1) / BK;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      int mb, nb;
+      decode(tile, g, mb, nb);
+      const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
+      const int w = args.weight_idx ? args.weight_idx[g] : g;
+      const int a_row = (int)(rs + (int64_t)mb * BM);
+      const int b_row = w * args.N + nb * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+          tma_load_2d(sa, &map_a, &full[stage], kb * BK, a_row);
+          tma_load_2d(sb, &map_b, &full[stage], kb * BK, b_row);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (lane 0 issues, whole warp waits)
+    constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const int num_kb = (args.K + BK - 1) / BK;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint8_t* sa = smem + stage * L::kStageBytes;
+          const uint8_t* sb = sa + L::kABytes;
+          const uint64_t adesc = make_sdesc_sw128(sa);
+          const uint64_t bdesc = make_sdesc_sw128(sb);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // advance 16 bf16 = 32 B along K inside the swizzle row (>>4 -> +2)
+            umma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+          }
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue warps 2..5
+    const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_in_tile = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int g = 0;
+    const int N = args.N;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      int mb, nb;
+      decode(tile, g, mb, nb);
+      const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
+      const int64_t rows_g = args.rows ? args.rows[g] : args.rows_const;
+      const int w = args.weight_idx ? args.weight_idx[g] : g;
+      const int64_t local_row = (int64_t)mb * BM + row_in_tile;
+      const bool valid = local_row < rows_g;
+      const int64_t out_row = rs + local_row;
+
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_addr = tmem_base + ((quarter * 32) << 16) + acc * BN;
+
+      if constexpr (EPI != EPI_GATE) {
+        const float* bias = args.bias ? args.bias + (int64_t)w * N : nullptr;
+        const bool vec_ok = (N % 8) == 0;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col0 = nb * BN + c * 32;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_addr + c * 32, r);
+          tmem_ld_wait();
+          if (!valid || col0 >= N) continue;
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v[i] = __uint_as_float(r[i]);
+            const int col = col0 + i;
+            if (bias != nullptr && col < N) v[i] += __ldg(bias + col);
+            if constexpr (EPI == EPI_BIAS_GELU) v[i] = gelu_tanh_fast(v[i]);
+          }
+          __nv_bfloat16* drow = args.D + out_row * N;
+          if (vec_ok && col0 + 32 <= N) {
+            uint4* dst = reinterpret_cast<uint4*>(drow + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 pk;
+              pk.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+              pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+              pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+              pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+              dst[q] = pk;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < N) drow[col0 + i] = __float2bfloat16_rn(v[i]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      } else {
+        // ---------------- gate epilogue: thread = token row, BN >= E columns
+        const int E = args.E;
+        const int64_t t = out_row;  // single group: rows are tokens
+        float b1 = -INFINITY, b2 = -INFINITY;
+        int i1 = 0x7fffffff, i2 = 0x7fffffff;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_addr + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int col = c * 32 + i;
+            const float v = __uint_as_float(r[i]);
+            if (col < E) {
+              // ascending column order + strict compare keeps lower index on ties
+              if (v > b1) {
+                b2 = b1; i2 = i1; b1 = v; i1 = col;
+              } else if (v > b2) {
+                b2 = v; i2 = col;
+              }
+            }
+          }
+          if (valid && args.logits != nullptr) {
+            float* lrow = args.logits + t * E;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i < E) lrow[c * 32 + i] = __uint_as_float(r[i]);
+          }
+        }
+        float sum = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_addr + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i < E) sum += expf(__uint_as_float(r[i]) - b1);
+        }
+        // accumulator consumed: hand TMEM back to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+
+        const int k = args.k;
+        int e0 = valid ? i1 : -1;
+        int e1 = (valid && k == 2) ? i2 : -2;
+        if (valid) {
+          args.ids[t * k] = i1;
+          args.gate_probs[t * k] = 1.0f / sum;  // exp(b1 - b1) / sum
+          if (k == 2) {
+            args.ids[t * k + 1] = i2;
+            args.gate_probs[t * k + 1] = expf(b2 - b1) / sum;
+          }
+        }
+        // per-tile capacity ranks (token-major order, gating.py:226)
+        // 4 x E per-warp counters in the tile-table region (G == 1 uses [0, 2))
+        int* wc = reinterpret_cast<int*>(smem + L::kTileOff) + 8;
+        const int tid = (warp - 2) * 32 + lane;  // 0..127
+        for (int i = tid; i < 4 * E; i += 128) wc[i] = 0;
+        named_bar_sync(1, 128);
+        int r0 = 0, r1 = 0;
+        if (k == 1) {
+          unsigned m = __match_any_sync(0xffffffffu, e0);
+          r0 = __popc(m & ((1u << lane) - 1u));
+        } else {
+          for (int l = 0; l < 32; ++l) {
+            int o0 = __shfl_sync(0xffffffffu, e0, l);
+            int o1 = __shfl_sync(0xffffffffu, e1, l);
+            if (l < (int)lane) {
+              r0 += (o0 == e0) + (o1 == e0);
+              r1 += (o0 == e1) + (o1 == e1);
+            }
+          }
+        }
+        if (valid) {
+          atomicAdd(&wc[quarter * E + e0], 1);
+          if (k == 2) atomicAdd(&wc[quarter * E + e1], 1);
+        }
+        named_bar_sync(1, 128);
+        if (valid) {
+          for (uint32_t q = 0; q < quarter; ++q) {
+            r0 += wc[q * E + e0];
+            if (k == 2) r1 += wc[q * E + e1];
+          }
+          args.local_rank[t * k] = r0;
+          if (k == 2) args.local_rank[t * k + 1] = r1;
+        }
+        for (int e = tid; e < E; e += 128)
+          args.tile_counts[(int64_t)mb * E + e] = wc[e] + wc[E + e] + wc[2 * E + e] + wc[3 * E + e];
+        named_bar_sync(1, 128);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, tmem_cols<BN>());
+  }
+}
+
+// ============================================================ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, cols] tensor map, box [box_rows, 64 cols], 128B swizzle.
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return MOE_ENODRV;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(cols * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : MOE_ETMA;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, int STAGES, int EPI>
+static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
+                     int64_t max_tiles, cudaStream_t st) {
+  using L = Smem<BN, STAGES>;
+  auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    if (e != cudaSuccess) return (int)e;
+    attr_done = true;
+  }
+  int grid = num_sms();
+  if (max_tiles < grid) grid = (int)(max_tiles < 1 ? 1 : max_tiles);
+  kern<<<grid, kThreads, L::kTotal, st>>>(ma, mb, args);
+  return (int)cudaGetLastError();
+}
+
+int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
+                             int N, const float* bias, void* D, int G, const int32_t* row_start,
+                             int64_t row_stride, const int32_t* rows, int64_t rows_const,
+                             const int32_t* weight_idx, int64_t max_group_rows, int act,
+                             cudaStream_t st) {
+  if (G < 1 || G > kMaxGroups || K < 1 || N < 1 || (K % 8) != 0) return MOE_EINVAL;
+  int BN = 256;
+  if (N <= 32) BN = 32;
+  else if (N <= 64) BN = 64;
+  else if (N <= 128) BN = 128;
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, A, a_rows, K, BM);
+  if (rc) return rc;
+  rc = make_map(&mb, B, b_rows, K, BN);
+  if (rc) return rc;
+  GemmArgs a{};
+  a.bias = bias;
+  a.D = (__nv_bfloat16*)D;
+  a.K = K;
+  a.N = N;
+  a.G = G;
+  a.row_start = row_start;
+  a.row_stride = row_stride;
+  a.rows = rows;
+  a.rows_const = rows_const;
+  a.weight_idx = weight_idx;
+  const int64_t nblk = (N + BN - 1) / BN;
+  const int64_t max_tiles = (int64_t)G * ((max_group_rows + BM - 1) / BM) * nblk;
+  if (max_tiles == 0) return 0;
+  const bool gelu = act == 1;
+#define MOE_TC(BN_, ST_)                                                            \
+  return gelu ? launch_tc<BN_, ST_, EPI_BIAS_GELU>(ma, mb, a, max_tiles, st)        \
+              : launch_tc<BN_, ST_, EPI_BIAS>(ma, mb, a, max_tiles, st)
+  switch (BN) {
+    case 32: MOE_TC(32, 8);
+    case 64: MOE_TC(64, 8);
+    case 128: MOE_TC(128, 6);
+    default: MOE_TC(256, 4);
+  }
+#undef MOE_TC
+}
+
+int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
+                          float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,
+                          int32_t* tile_counts, cudaStream_t st) {
+  if (S == 0) return 0;
+  if (E < 1 || E > 256 || (M % 8) != 0 || k < 1 || k > 2) return MOE_EINVAL;
+  int BN = 32;
+  while (BN < E) BN *= 2;
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, x, S, M, BM);
+  if (rc) return rc;
+  rc = make_map(&mb, wg_t, BN, M, BN);  // wg_t is padded to BN rows
+  if (rc) return rc;
+  GemmArgs a{};
+  a.K = M;
+  a.N = BN;
+  a.G = 1;
+  a.row_stride = 0;
+  a.rows_const = S;
+  a.E = E;
+  a.k = k;
+  a.S = S;
+  a.logits = logits;
+  a.ids = ids;
+  a.gate_probs = gate_probs;
+  a.local_rank = local_rank;
+  a.tile_counts = tile_counts;
+  const int64_t tiles = (S + BM - 1) / BM;
+  switch (BN) {
+    case 32: return launch_tc<32, 8, EPI_GATE>(ma, mb, a, tiles, st);
+    case 64: return launch_tc<64, 8, EPI_GATE>(ma, mb, a, tiles, st);
+    case 128: return launch_tc<128, 6, EPI_GATE>(ma, mb, a, tiles, st);
+    default: return launch_tc<256, 4, EPI_GATE>(ma, mb, a, tiles, st);
+  }
+}
+
+}  // namespace moe

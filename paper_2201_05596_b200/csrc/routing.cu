@@ -1,0 +1,549 @@
+// Routing kernels for the MoE layer forward on sm_100a:
+//   * top-k gate from logits (softmax + arg-max with lower-index ties)
+//   * plan tiles  : per-128-token-tile local ranks + per-expert tile counts
+//   * plan scan   : per-expert exclusive scan over tiles (+ EP rank offsets)
+//   * plan slots  : slot = tile offset + local rank, DROPPED past capacity
+//   * int64 exclusive scan and the Blelloch tree-order f64 scan
+//   * table-driven scatter (dispatch) and combine
+//
+// Reference semantics: /root/reference/pkg/src/moekit/gating.py:142-307 and
+// arch.py:372-413. All integer outputs are bit-exact with the reference.
+#include "common.cuh"
+#include "moe_kernels.h"
+
+namespace moe {
+
+// ============================================================ top-k gate
+// One warp per token row. Lane l owns columns l, l+32, ... (coalesced).
+template <typename T>
+MOE_DEV void better(T v, int i, T& bv, int& bi) {
+  // descending value, ties to the lower expert index (gating.py:159-161)
+  if (v > bv || (v == bv && i < bi)) {
+    bv = v;
+    bi = i;
+  }
+}
+
+template <typename T>
+MOE_DEV void warp_argmax(T& v, int& i) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    T ov = __shfl_xor_sync(0xffffffffu, v, off);
+    int oi = __shfl_xor_sync(0xffffffffu, i, off);
+    better(ov, oi, v, i);
+  }
+}
+
+MOE_DEV float exp_t(float x) { return expf(x); }
+MOE_DEV double exp_t(double x) { return exp(x); }
+
+template <typename T>
+__global__ void topk_gate_kernel(const T* __restrict__ logits, int64_t S, int E, int k,
+                                 int32_t* __restrict__ ids, T* __restrict__ gate_probs,
+                                 T* __restrict__ probs) {
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
+       t += warps_total) {
+    const T* row = logits + t * E;
+    const T ninf = -INFINITY;
+    T b1 = ninf;
+    int i1 = 0x7fffffff;
+    for (int c = lane; c < E; c += 32) better(row[c], c, b1, i1);
+    warp_argmax(b1, i1);
+    T b2 = ninf;
+    int i2 = 0x7fffffff;
+    if (k == 2) {
+      for (int c = lane; c < E; c += 32)
+        if (c != i1) better(row[c], c, b2, i2);
+      warp_argmax(b2, i2);
+    }
+    // max-shifted softmax over all E columns (gating.py:156-158)
+    T m = b1;
+    T sum = 0;
+    for (int c = lane; c < E; c += 32) sum += exp_t(row[c] - m);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if (probs != nullptr)
+      for (int c = lane; c < E; c += 32) probs[t * E + c] = exp_t(row[c] - m) / sum;
+    if (lane == 0) {
+      ids[t * k] = i1;
+      gate_probs[t * k] = exp_t(b1 - m) / sum;
+      if (k == 2) {
+        ids[t * k + 1] = i2;
+        gate_probs[t * k + 1] = exp_t(b2 - m) / sum;
+      }
+    }
+  }
+}
+
+// ============================================================ plan: tiles
+// Block = one routing tile of 128 tokens, thread = token. local_rank[t, j] is
+// the number of earlier assignments (token-major, gating.py:226) to the same
+// expert inside the tile; tile_counts[tile, e] the tile's assignments to e.
+MOE_DEV int warp_rank_same(int key, int my_lane) {
+  unsigned m = __match_any_sync(0xffffffffu, key);
+  return __popc(m & ((1u << my_lane) - 1u));
+}
+
+__global__ void plan_tiles_kernel(const int32_t* __restrict__ ids, int64_t S, int k, int E,
+                                  int32_t* __restrict__ local_rank,
+                                  int32_t* __restrict__ tile_counts) {
+  extern __shared__ int cnt[];  // [4][E]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t tile = blockIdx.x;
+  const int64_t t = tile * kRouteTile + tid;
+  for (int i = tid; i < 4 * E; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const bool valid = t < S;
+  int e0 = valid ? ids[t * k] : -1;
+  int e1 = (valid && k == 2) ? ids[t * k + 1] : -2;
+  int r0 = 0, r1 = 0;
+  if (k == 1) {
+    r0 = warp_rank_same(e0, lane);
+  } else {
+    for (int l = 0; l < 32; ++l) {
+      int o0 = __shfl_sync(0xffffffffu, e0, l);
+      int o1 = __shfl_sync(0xffffffffu, e1, l);
+      if (l < lane) {
+        r0 += (o0 == e0) + (o1 == e0);
+        r1 += (o0 == e1) + (o1 == e1);
+      }
+    }
+  }
+  if (valid) {
+    atomicAdd(&cnt[w * E + e0], 1);
+    if (k == 2) atomicAdd(&cnt[w * E + e1], 1);
+  }
+  __syncthreads();
+  if (valid) {
+    for (int q = 0; q < w; ++q) {
+      r0 += cnt[q * E + e0];
+      if (k == 2) r1 += cnt[q * E + e1];
+    }
+    local_rank[t * k] = r0;
+    if (k == 2) local_rank[t * k + 1] = r1;
+  }
+  for (int e = tid; e < E; e += blockDim.x)
+    tile_counts[tile * E + e] = cnt[e] + cnt[E + e] + cnt[2 * E + e] + cnt[3 * E + e];
+}
+
+// ============================================================ plan: scan
+// Block (32 experts x 32 chunks). tile_offsets[tile, e] = base[e] + sum of
+// tile_counts[t' < tile, e]; totals[e] = sum over tiles; kept[e] = how many of
+// this batch's assignments to e land below capacity given base[e].
+__global__ void plan_scan_kernel(const int32_t* __restrict__ tile_counts, int64_t T, int E,
+                                 int64_t cap, const int32_t* __restrict__ base,
+                                 int32_t* __restrict__ tile_offsets, int32_t* __restrict__ totals,
+                                 int32_t* __restrict__ kept) {
+  __shared__ int part[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int e = blockIdx.x * 32 + tx;
+  const int64_t chunk = (T + 31) / 32;
+  const int64_t lo = ty * chunk, hi = min(T, lo + chunk);
+  int s = 0;
+  if (e < E)
+    for (int64_t i = lo; i < hi; ++i) s += tile_counts[i * E + e];
+  part[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0) {
+    int run = (e < E && base != nullptr) ? base[e] : 0;
+    const int b0 = run;
+    for (int j = 0; j < 32; ++j) {
+      int v = part[j][tx];
+      part[j][tx] = run;
+      run += v;
+    }
+    if (e < E) {
+      const int total = run - b0;
+      totals[e] = total;
+      long long hi_kept = min((long long)run, (long long)cap);
+      long long k_ = hi_kept - b0;
+      kept[e] = (int)(k_ < 0 ? 0 : k_);
+    }
+  }
+  __syncthreads();
+  if (e < E) {
+    int run = part[ty][tx];
+    for (int64_t i = lo; i < hi; ++i) {
+      tile_offsets[i * E + e] = run;
+      run += tile_counts[i * E + e];
+    }
+  }
+}
+
+// ============================================================ plan: slots
+__global__ void plan_slots_kernel(const int32_t* __restrict__ ids,
+                                  const int32_t* __restrict__ local_rank,
+                                  const int32_t* __restrict__ tile_offsets, int64_t S, int k, int E,
+                                  int64_t cap, int32_t* __restrict__ slots) {
+  const int64_t n = S * k;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = a / k;
+    const int e = ids[a];
+    const int64_t slot = (int64_t)tile_offsets[(t / kRouteTile) * E + e] + local_rank[a];
+    slots[a] = slot < cap ? (int32_t)slot : -1;
+  }
+}
+
+// ============================================================ int64 scan
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanBlock = kScanThreads * kScanItems;
+
+template <bool kWriteOut>
+__global__ void scan_i64_block_kernel(const int64_t* __restrict__ in, int64_t n,
+                                      const int64_t* __restrict__ block_base,
+                                      int64_t* __restrict__ out, int64_t* __restrict__ block_sums) {
+  __shared__ int64_t warp_tot[kScanThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kScanBlock + (int64_t)tid * kScanItems;
+  int64_t v[kScanItems];
+  int64_t run = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t idx = base + i;
+    v[i] = idx < n ? in[idx] : 0;
+    const int64_t x = v[i];
+    v[i] = run;  // exclusive within thread
+    run += x;
+  }
+  // warp inclusive scan of per-thread totals
+  int64_t incl = run;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int64_t wt = lane < kScanThreads / 32 ? warp_tot[lane] : 0;
+    int64_t wi = wt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int64_t o = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += o;
+    }
+    if (lane < kScanThreads / 32) warp_tot[lane] = wi - wt;  // exclusive warp offsets
+    if (lane == kScanThreads / 32 - 1 && block_sums != nullptr) block_sums[blockIdx.x] = wi;
+  }
+  __syncthreads();
+  if (kWriteOut) {
+    const int64_t off = (incl - run) + warp_tot[w] + (block_base ? block_base[blockIdx.x] : 0);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      const int64_t idx = base + i;
+      if (idx < n) out[idx] = v[i] + off;
+    }
+  }
+}
+
+// ============================================================ Blelloch f64
+// One tree level of gating.py:189-201, applied with the same pairings so the
+// float result matches NumPy bit for bit (plain IEEE adds, no contraction).
+__global__ void blelloch_up_kernel(double* tree, int64_t m, int64_t d) {
+  const int64_t pairs = m / (2 * d);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = (2 * i + 2) * d - 1, l = (2 * i + 1) * d - 1;
+    tree[r] = __dadd_rn(tree[r], tree[l]);
+  }
+}
+
+__global__ void blelloch_down_kernel(double* tree, int64_t m, int64_t d) {
+  const int64_t pairs = m / (2 * d);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = (2 * i + 2) * d - 1, l = (2 * i + 1) * d - 1;
+    const double left = tree[l];
+    tree[l] = tree[r];
+    tree[r] = __dadd_rn(tree[r], left);
+  }
+}
+
+// ============================================================ scatter
+// Warp per token: the row is read once and stored to each kept (expert, slot)
+// of the token. With local_rank/tile_offsets given, the slot is resolved here
+// (and written to slots) - the layer path fuses plan_slots into dispatch.
+template <typename V>
+__global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t S, int64_t row_bytes, int k,
+                               int E, int64_t cap, const int32_t* __restrict__ ids,
+                               int32_t* __restrict__ slots, const int32_t* __restrict__ local_rank,
+                               const int32_t* __restrict__ tile_offsets, uint8_t* __restrict__ buf,
+                               uint8_t* __restrict__ occupied) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t nvec = row_bytes / (int64_t)sizeof(V);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
+       t += warps_total) {
+    int64_t dst_row[2] = {-1, -1};
+    for (int j = 0; j < k; ++j) {
+      const int e = ids[t * k + j];
+      int64_t slot;
+      if (local_rank != nullptr) {
+        slot = (int64_t)tile_offsets[(t / kRouteTile) * E + e] + local_rank[t * k + j];
+        if (slot >= cap) slot = -1;
+        if (lane == 0) slots[t * k + j] = (int32_t)slot;
+      } else {
+        slot = slots[t * k + j];
+      }
+      if (slot >= 0) {
+        dst_row[j] = (int64_t)e * cap + slot;
+        if (occupied != nullptr && lane == 0) occupied[dst_row[j]] = 1;
+      }
+    }
+    if (dst_row[0] < 0 && dst_row[1] < 0) continue;
+    const V* src = reinterpret_cast<const V*>(x + t * row_bytes);
+    V* d0 = dst_row[0] >= 0 ? reinterpret_cast<V*>(buf + dst_row[0] * row_bytes) : nullptr;
+    V* d1 = dst_row[1] >= 0 ? reinterpret_cast<V*>(buf + dst_row[1] * row_bytes) : nullptr;
+    constexpr int U = 4;
+    int64_t i = lane;
+    for (; i + 32 * (U - 1) < nvec; i += 32 * U) {
+      V r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) r[u] = __ldg(src + i + 32 * u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (d0) d0[i + 32 * u] = r[u];
+        if (d1) d1[i + 32 * u] = r[u];
+      }
+    }
+    for (; i < nvec; i += 32) {
+      V r = __ldg(src + i);
+      if (d0) d0[i] = r;
+      if (d1) d1[i] = r;
+    }
+  }
+}
+
+// ============================================================ combine
+template <typename T>
+struct Acc {
+  using type = float;
+};
+template <>
+struct Acc<double> {
+  using type = double;
+};
+
+MOE_DEV float to_acc(float v) { return v; }
+MOE_DEV float to_acc(__nv_bfloat16 v) { return __bfloat162float(v); }
+MOE_DEV double to_acc(double v) { return v; }
+template <typename T>
+MOE_DEV T from_acc(float v);
+template <>
+MOE_DEV float from_acc<float>(float v) {
+  return v;
+}
+template <>
+MOE_DEV __nv_bfloat16 from_acc<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+MOE_DEV double from_acc_d(double v) { return v; }
+
+MOE_DEV float add_rn(float a, float b) { return __fadd_rn(a, b); }
+MOE_DEV double add_rn(double a, double b) { return __dadd_rn(a, b); }
+MOE_DEV float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+MOE_DEV double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+// out[t] = (x[t] + sum_j p_j * y[row_j]) + shared[t]   (arch.py:389-391, :406-410)
+// kExpertOrder: contributions summed in ascending expert id (forward_layer's
+// loop over experts); otherwise in choice order (combine_tokens' np.add.at).
+// Every multiply/add is individually rounded so f64 results match NumPy.
+template <typename T, typename P, bool kExpertOrder>
+__global__ void combine_kernel(const T* __restrict__ y, int64_t S, int M, int k, int E, int64_t cap,
+                               const int32_t* __restrict__ ids, const int32_t* __restrict__ slots,
+                               const int32_t* __restrict__ row_index, const P* __restrict__ gp,
+                               const T* __restrict__ x, const T* __restrict__ shared,
+                               T* __restrict__ out) {
+  using A = typename Acc<T>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
+       t += warps_total) {
+    int64_t row[2] = {-1, -1};
+    A p[2] = {0, 0};
+    int ex[2] = {0, 0};
+    int n = 0;
+    for (int j = 0; j < k; ++j) {
+      int64_t r;
+      if (row_index != nullptr) {
+        r = row_index[t * k + j];
+      } else {
+        const int s = slots[t * k + j];
+        r = s >= 0 ? (int64_t)ids[t * k + j] * cap + s : -1;
+      }
+      if (r >= 0) {
+        row[n] = r;
+        p[n] = (A)gp[t * k + j];
+        ex[n] = ids[t * k + j];
+        ++n;
+      }
+    }
+    if (kExpertOrder && n == 2 && ex[1] < ex[0]) {
+      int64_t tr = row[0]; row[0] = row[1]; row[1] = tr;
+      A tp = p[0]; p[0] = p[1]; p[1] = tp;
+    }
+    for (int c = lane; c < M; c += 32) {
+      A acc = 0;  // the zero accumulator of scatter_rows / np.add.at
+      for (int i = 0; i < n; ++i) acc = add_rn(acc, mul_rn(p[i], to_acc(y[row[i] * M + c])));
+      A o = acc;
+      if (x != nullptr) o = add_rn(to_acc(x[t * M + c]), acc);
+      if (shared != nullptr) o = add_rn(o, to_acc(shared[t * M + c]));
+      if constexpr (sizeof(T) == 8) {
+        out[t * M + c] = o;
+      } else {
+        out[t * M + c] = from_acc<T>(o);
+      }
+    }
+  }
+}
+
+// ============================================================ launchers
+static int grid_for(int64_t work, int per_block, int cap_blocks = 148 * 32) {
+  int64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap_blocks) g = cap_blocks;
+  return (int)g;
+}
+
+int launch_topk_gate(const void* logits, int dtype, int64_t S, int E, int k, int32_t* ids,
+                     void* gate_probs, void* probs, cudaStream_t st) {
+  if (S == 0) return 0;
+  const int threads = 256;
+  const int g = grid_for(S, threads / 32, 148 * 64);
+  if (dtype == MOE_F32)
+    topk_gate_kernel<float><<<g, threads, 0, st>>>((const float*)logits, S, E, k, ids,
+                                                   (float*)gate_probs, (float*)probs);
+  else if (dtype == MOE_F64)
+    topk_gate_kernel<double><<<g, threads, 0, st>>>((const double*)logits, S, E, k, ids,
+                                                    (double*)gate_probs, (double*)probs);
+  else
+    return MOE_EINVAL;
+  return (int)cudaGetLastError();
+}
+
+int launch_plan(const int32_t* ids, int64_t S, int k, int E, int64_t cap, const int32_t* base,
+                int32_t* local_rank, int32_t* tile_counts, int32_t* tile_offsets, int32_t* totals,
+                int32_t* kept, int32_t* slots, bool tiles, bool scan, bool do_slots,
+                cudaStream_t st) {
+  const int64_t T = (S + kRouteTile - 1) / kRouteTile;
+  if (tiles && T > 0) {
+    plan_tiles_kernel<<<(unsigned)T, kRouteTile, 4 * E * sizeof(int), st>>>(ids, S, k, E,
+                                                                           local_rank, tile_counts);
+  }
+  if (scan) {
+    dim3 blk(32, 32);
+    plan_scan_kernel<<<(E + 31) / 32, blk, 0, st>>>(tile_counts, T, E, cap, base, tile_offsets,
+                                                    totals, kept);
+  }
+  if (do_slots && S > 0) {
+    plan_slots_kernel<<<grid_for(S * k, 256), 256, 0, st>>>(ids, local_rank, tile_offsets, S, k, E,
+                                                            cap, slots);
+  }
+  return (int)cudaGetLastError();
+}
+
+int64_t scan_i64_workspace_elems(int64_t n) {
+  int64_t total = 0;
+  while (n > kScanBlock) {
+    n = (n + kScanBlock - 1) / kScanBlock;
+    total += 2 * n;
+  }
+  return total + 1;
+}
+
+static void scan_i64_rec(const int64_t* in, int64_t n, int64_t* out, int64_t* ws,
+                         cudaStream_t st) {
+  const int64_t blocks = (n + kScanBlock - 1) / kScanBlock;
+  if (blocks <= 1) {
+    scan_i64_block_kernel<true><<<1, kScanThreads, 0, st>>>(in, n, nullptr, out, nullptr);
+    return;
+  }
+  int64_t* sums = ws;
+  int64_t* sums_scan = ws + blocks;
+  scan_i64_block_kernel<false><<<(unsigned)blocks, kScanThreads, 0, st>>>(in, n, nullptr, nullptr,
+                                                                          sums);
+  scan_i64_rec(sums, blocks, sums_scan, ws + 2 * blocks, st);
+  scan_i64_block_kernel<true><<<(unsigned)blocks, kScanThreads, 0, st>>>(in, n, sums_scan, out,
+                                                                         nullptr);
+}
+
+int launch_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* ws, cudaStream_t st) {
+  if (n == 0) return 0;
+  scan_i64_rec(in, n, out, ws, st);
+  return (int)cudaGetLastError();
+}
+
+int launch_blelloch_f64(double* tree, int64_t m, cudaStream_t st) {
+  // tree holds the zero-padded input (m a power of two); exclusive scan in place
+  for (int64_t d = 1; d < m; d <<= 1)
+    blelloch_up_kernel<<<grid_for(m / (2 * d), 256), 256, 0, st>>>(tree, m, d);
+  cudaMemsetAsync(tree + (m - 1), 0, sizeof(double), st);
+  for (int64_t d = m >> 1; d >= 1; d >>= 1)
+    blelloch_down_kernel<<<grid_for(m / (2 * d), 256), 256, 0, st>>>(tree, m, d);
+  return (int)cudaGetLastError();
+}
+
+int launch_scatter(const void* x, int64_t S, int64_t row_bytes, int k, int E, int64_t cap,
+                   const int32_t* ids, int32_t* slots, const int32_t* local_rank,
+                   const int32_t* tile_offsets, void* buf, uint8_t* occupied, cudaStream_t st) {
+  if (S == 0) return 0;
+  const int threads = 256;
+  const int g = grid_for(S, threads / 32, 148 * 64);
+  const uint8_t* xb = (const uint8_t*)x;
+  uint8_t* bb = (uint8_t*)buf;
+  if (row_bytes % 16 == 0)
+    scatter_kernel<uint4><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots,
+                                                 local_rank, tile_offsets, bb, occupied);
+  else if (row_bytes % 8 == 0)
+    scatter_kernel<uint2><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots,
+                                                 local_rank, tile_offsets, bb, occupied);
+  else if (row_bytes % 4 == 0)
+    scatter_kernel<uint32_t><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots,
+                                                    local_rank, tile_offsets, bb, occupied);
+  else
+    scatter_kernel<uint16_t><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots,
+                                                    local_rank, tile_offsets, bb, occupied);
+  return (int)cudaGetLastError();
+}
+
+template <typename T, typename P>
+static void combine_dispatch(bool expert_order, int g, int threads, cudaStream_t st, const void* y,
+                             int64_t S, int M, int k, int E, int64_t cap, const int32_t* ids,
+                             const int32_t* slots, const int32_t* row_index, const void* gp,
+                             const void* x, const void* shared, void* out) {
+  if (expert_order)
+    combine_kernel<T, P, true><<<g, threads, 0, st>>>((const T*)y, S, M, k, E, cap, ids, slots,
+                                                      row_index, (const P*)gp, (const T*)x,
+                                                      (const T*)shared, (T*)out);
+  else
+    combine_kernel<T, P, false><<<g, threads, 0, st>>>((const T*)y, S, M, k, E, cap, ids, slots,
+                                                       row_index, (const P*)gp, (const T*)x,
+                                                       (const T*)shared, (T*)out);
+}
+
+int launch_combine(const void* y, int dtype, int64_t S, int M, int k, int E, int64_t cap,
+                   const int32_t* ids, const int32_t* slots, const int32_t* row_index,
+                   const void* gate_probs, int gp_dtype, const void* x, const void* shared,
+                   void* out, int expert_order, cudaStream_t st) {
+  if (S == 0) return 0;
+  const int threads = 256;
+  const int g = grid_for(S, threads / 32, 148 * 64);
+  if (dtype == MOE_F64 && gp_dtype == MOE_F64)
+    combine_dispatch<double, double>(expert_order, g, threads, st, y, S, M, k, E, cap, ids, slots,
+                                     row_index, gate_probs, x, shared, out);
+  else if (dtype == MOE_F32 && gp_dtype == MOE_F32)
+    combine_dispatch<float, float>(expert_order, g, threads, st, y, S, M, k, E, cap, ids, slots,
+                                   row_index, gate_probs, x, shared, out);
+  else if (dtype == MOE_BF16 && gp_dtype == MOE_F32)
+    combine_dispatch<__nv_bfloat16, float>(expert_order, g, threads, st, y, S, M, k, E, cap, ids,
+                                           slots, row_index, gate_probs, x, shared, out);
+  else
+    return MOE_EINVAL;
+  return (int)cudaGetLastError();
+}
+
+}  // namespace moe

@@ -1,0 +1,112 @@
+"""Numerics of the grouped GEMM kernels against a plain PyTorch reference
+(fp32 / fp64 math on the same bf16- or fp32-rounded operands)."""
+
+import pytest
+import torch
+
+from paper_2201_05596_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _gelu(x):
+    return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def _ref(a, w_t, bias, rows, starts, widx, act, N):
+    """fp32 reference: for group g, D[rows] = act(A[rows] @ W_w^T + b_w)."""
+    out = {}
+    for g, (r, s) in enumerate(zip(rows, starts)):
+        if r == 0:
+            continue
+        wi = widx[g]
+        w = w_t[wi * N:(wi + 1) * N].float()
+        y = a[s:s + r].float() @ w.t()
+        if bias is not None:
+            y = y + bias[wi]
+        out[g] = _gelu(y) if act else y
+    return out
+
+
+@pytest.mark.parametrize("K,N,act", [(1024, 4096, 1), (4096, 1024, 0), (2048, 8192, 1),
+                                     (64, 256, 0), (16, 64, 1), (136, 200, 0), (2048, 96, 1)])
+def test_grouped_gemm_bf16(K, N, act):
+    torch.manual_seed(K + N)
+    G, cap = 5, 300
+    rows = [300, 0, 129, 1, 257]
+    starts = [g * cap for g in range(G)]
+    a = (torch.randn(G * cap, K, device="cuda") * 0.5).to(torch.bfloat16)
+    w_t = (torch.randn(G * N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(G, N, device="cuda") * 0.1
+    d = torch.full((G * cap, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    rows_t = torch.tensor(rows, dtype=torch.int32, device="cuda")
+    _lib.call("moe_grouped_gemm_bf16", a.data_ptr(), G * cap, K, w_t.data_ptr(), G * N, N,
+              bias.data_ptr(), d.data_ptr(), G, None, cap, rows_t.data_ptr(), 0, None, cap, act,
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    ref = _ref(a, w_t, bias, rows, starts, list(range(G)), act, N)
+    for g, want in ref.items():
+        got = d[starts[g]:starts[g] + rows[g]].float()
+        scale = want.abs().mean().item() + 1e-6
+        err = (got - want).abs().max().item()
+        assert err <= 2e-2 * (want.abs().max().item() + scale), (g, err)
+    # rows beyond each group's count are untouched
+    assert torch.isnan(d[cap:2 * cap].float()).all()
+    assert torch.isnan(d[2 * cap + 129:3 * cap].float()).all()
+
+
+def test_grouped_gemm_bf16_weight_index_and_row_start():
+    torch.manual_seed(0)
+    K, N = 512, 512
+    rows = [200, 64, 333]
+    starts = [17, 500, 700]
+    widx = [2, 0, 2]
+    a = torch.randn(1100, K, device="cuda").to(torch.bfloat16)
+    w_t = (torch.randn(3 * N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    d = torch.zeros(1100, N, device="cuda", dtype=torch.bfloat16)
+    t = lambda v: torch.tensor(v, dtype=torch.int32, device="cuda")  # noqa: E731
+    rs, rw, wi = t(starts), t(rows), t(widx)
+    _lib.call("moe_grouped_gemm_bf16", a.data_ptr(), 1100, K, w_t.data_ptr(), 3 * N, N, None,
+              d.data_ptr(), 3, rs.data_ptr(), 0, rw.data_ptr(), 0, wi.data_ptr(), 333, 0,
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    ref = _ref(a, w_t, None, rows, starts, widx, 0, N)
+    for g, want in ref.items():
+        got = d[starts[g]:starts[g] + rows[g]].float()
+        assert (got - want).abs().max().item() <= 2e-2 * want.abs().max().item()
+
+
+def test_grouped_gemm_bf16_many_tiles_persistent():
+    # more tiles than SMs, uniform groups: exercises the persistent scheduler
+    torch.manual_seed(1)
+    G, cap, K, N = 16, 640, 1024, 1024
+    a = torch.randn(G * cap, K, device="cuda").to(torch.bfloat16)
+    w_t = (torch.randn(G * N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    d = torch.empty(G * cap, N, device="cuda", dtype=torch.bfloat16)
+    _lib.call("moe_grouped_gemm_bf16", a.data_ptr(), G * cap, K, w_t.data_ptr(), G * N, N, None,
+              d.data_ptr(), G, None, cap, None, cap, None, cap, 0, _lib.stream_ptr())
+    want = torch.bmm(a.view(G, cap, K).float(), w_t.view(G, N, K).float().transpose(1, 2))
+    got = d.view(G, cap, N).float()
+    assert (got - want).abs().max().item() <= 2e-2 * want.abs().max().item()
+
+
+@pytest.mark.parametrize("K,N,act", [(1024, 4096, 1), (4096, 1024, 0), (8, 8, 1), (33, 17, 0)])
+def test_grouped_gemm_f32(K, N, act):
+    torch.manual_seed(K)
+    G, cap = 3, 200
+    rows = [200, 5, 0]
+    a = torch.randn(G * cap, K, device="cuda")
+    w = torch.randn(G, K, N, device="cuda") / K ** 0.5
+    bias = torch.randn(G, N, device="cuda")
+    d = torch.zeros(G * cap, N, device="cuda")
+    rows_t = torch.tensor(rows, dtype=torch.int32, device="cuda")
+    _lib.call("moe_grouped_gemm_f32", a.data_ptr(), K, w.data_ptr(), N, bias.data_ptr(),
+              d.data_ptr(), G, None, cap, rows_t.data_ptr(), 0, None, cap, act, _lib.stream_ptr())
+    for g, r in enumerate(rows):
+        if r == 0:
+            continue
+        want = a[g * cap:g * cap + r].double() @ w[g].double() + bias[g].double()
+        if act:
+            want = _gelu(want)
+        got = d[g * cap:g * cap + r].double()
+        assert ((got - want).abs() <= 1e-5 * (want.abs() + want.abs().mean())).all()

@@ -1,0 +1,258 @@
+"""Layer-forward parity: the B200 MoE layer against the CPU oracle.
+
+Protocol: inputs and weights are rounded to the device dtype
+and the same rounded values (in float64) go to the oracle; routing is
+compared on the GPU's own gate logits (fp32, exactly representable in f64),
+so ids/slots/drops must be bit-exact and the outputs must agree within
+    |got - want| <= rtol * (|want| + RMS(want))
+with rtol = 1e-5 (fp32) and 2e-2 (bf16): the RMS term is the atol for
+near-zero entries (written down once here and in DESIGN.md).
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_oracle as O
+from paper_2201_05596_b200 import arch as A
+from paper_2201_05596_b200.gating import GatingConfig
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def close(got, want, rtol):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    rms = float(np.sqrt(np.mean(want ** 2))) if want.size else 0.0
+    err = np.abs(got - want)
+    bound = rtol * (np.abs(want) + rms)
+    worst = float(np.max(err - bound)) if want.size else -1.0
+    assert worst <= 0.0, f"max excess {worst:.3e} (max err {err.max():.3e}, rms {rms:.3e})"
+
+
+def rounded_params(spec, seed, dtype, bias_scale=0.05):
+    """Reference-initialised params, biases randomised, rounded to dtype."""
+    rng = np.random.default_rng(seed)
+    p = A.init_layer_params(spec, rng)
+    for f in list(p.experts) + ([p.shared] if p.shared else []):
+        f.b1.value[:] = rng.standard_normal(f.b1.value.shape) * bias_scale
+        f.b2.value[:] = rng.standard_normal(f.b2.value.shape) * bias_scale
+    tdt = torch.bfloat16 if dtype == torch.bfloat16 else torch.float32
+
+    def r(a):
+        return torch.as_tensor(a).to(tdt).double().numpy()
+
+    p.gate_w.value[:] = r(p.gate_w.value)
+    for f in list(p.experts) + ([p.shared] if p.shared else []):
+        f.w1.value[:] = r(f.w1.value)
+        f.w2.value[:] = r(f.w2.value)
+        f.b1.value[:] = torch.as_tensor(f.b1.value).float().double().numpy()
+        f.b2.value[:] = torch.as_tensor(f.b2.value).float().double().numpy()
+    return p
+
+
+def oracle_args(p):
+    experts = [(f.w1.value, f.b1.value, f.w2.value, f.b2.value) for f in p.experts]
+    shared = None if p.shared is None else (p.shared.w1.value, p.shared.b1.value,
+                                            p.shared.w2.value, p.shared.b2.value)
+    return experts, shared
+
+
+def run_layer(spec, p, x64, dtype):
+    layer = A.MoeLayer(spec, p, dtype=dtype)
+    x = torch.as_tensor(x64).to(device="cuda", dtype=dtype)
+    logits = torch.empty((x.shape[0], spec.experts), dtype=torch.float32, device="cuda")
+    out = layer(x, logits_out=logits)
+    torch.cuda.synchronize()
+    return layer, x, out, logits
+
+
+def check_routing(layer, logits, spec, S):
+    ids, gp, slots, load, cap = layer.plan(S)
+    lg = logits.double().cpu().numpy()
+    ids_ref, gp_ref, _ = O.top_k_gate(lg, spec.experts, spec.gating.k)
+    assert np.array_equal(ids.cpu().numpy(), ids_ref)
+    np.testing.assert_allclose(gp.cpu().numpy(), gp_ref, rtol=2e-6, atol=1e-30)
+    s_ref, l_ref, c_ref = O.build_dispatch_plan_fast(ids_ref, spec.experts, spec.gating.k,
+                                                     spec.gating.capacity_factor)
+    assert cap == c_ref
+    assert np.array_equal(slots.cpu().numpy(), s_ref)
+    assert np.array_equal(load.cpu().numpy(), l_ref)
+    return lg, s_ref
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_golden_layers(dtype):
+    """Every golden layer case (made by the reference): fp32 path against the
+    reference output directly; both paths against the oracle on GPU logits."""
+    z = np.load(os.path.join(GOLDEN, "layers.npz"))
+    for i in range(int(z["n"])):
+        s, m, e, k, cf, res = z[f"l{i}_cfg"]
+        s, m, e, k = int(s), int(m), int(e), int(k)
+        if dtype == torch.bfloat16 and m % 8:
+            continue
+        spec = A.LayerSpec(kind="moe", hidden=m, experts=e, residual=bool(res),
+                           gating=GatingConfig(e, k, float(cf)))
+        experts = [A.FfnParams(*(A.Tensor(z[f"l{i}_{n}"][j]) for n in ("w1", "b1", "w2", "b2")))
+                   for j in range(e)]
+        shared = None
+        if res:
+            shared = A.FfnParams(*(A.Tensor(z[f"l{i}_{n}"]) for n in ("sw1", "sb1", "sw2", "sb2")))
+        p = A.MoeLayerParams(gate_w=A.Tensor(z[f"l{i}_gate_w"]), experts=tuple(experts),
+                             shared=shared)
+        x64 = z[f"l{i}_x"]
+        if dtype == torch.float32:
+            got = A.forward_layer(x64, spec, p)  # NumPy in -> fp32 device path -> NumPy out
+            close(got, z[f"l{i}_out"], 1e-5)
+            continue
+        # bf16: round inputs/weights, compare with the oracle on the same values
+        rx = torch.as_tensor(x64).to(torch.bfloat16).double().numpy()
+        for f in list(p.experts) + ([p.shared] if p.shared else []):
+            for leaf in (f.w1, f.w2):
+                leaf.value[:] = torch.as_tensor(leaf.value).to(torch.bfloat16).double().numpy()
+        p.gate_w.value[:] = torch.as_tensor(p.gate_w.value).to(torch.bfloat16).double().numpy()
+        layer, x, out, logits = run_layer(spec, p, rx, dtype)
+        lg, _ = check_routing(layer, logits, spec, s)
+        ex, sh = oracle_args(p)
+        want = O.forward_layer_with_logits(rx, lg, ex, sh, e, k, float(cf))
+        close(out.float().cpu().numpy(), want, 2e-2)
+
+
+def test_dropped_tokens_ride_skip_bitwise():
+    # test_arch.py:267-275: capacity 1 per expert, everything else == x exactly
+    for dtype in (torch.float32, torch.bfloat16):
+        spec = A.LayerSpec(kind="moe", hidden=64, experts=2, gating=GatingConfig(2, 1, 1e-9))
+        p = rounded_params(spec, 24, dtype)
+        x64 = torch.randn(300, 64, generator=torch.Generator().manual_seed(3)).to(dtype).double().numpy()
+        layer, x, out, logits = run_layer(spec, p, x64, dtype)
+        _, slots = check_routing(layer, logits, spec, 300)
+        dropped = (slots < 0).all(axis=1)
+        assert dropped.sum() >= 298
+        assert torch.equal(out[torch.as_tensor(dropped, device="cuda")],
+                           x[torch.as_tensor(dropped, device="cuda")])
+
+
+def test_zero_experts_residual_is_x_plus_mlp():
+    # test_arch.py:232-242
+    spec = A.LayerSpec(kind="moe", hidden=32, experts=3, residual=True,
+                       gating=GatingConfig(3, 1, 8.0))
+    p = rounded_params(spec, 21, torch.float32)
+    for f in p.experts:
+        for leaf in f.leaves():
+            leaf.value[:] = 0.0
+    x64 = np.random.default_rng(21).standard_normal((6, 32))
+    got = A.forward_layer(x64, spec, p)
+    want = x64 + O.forward_ffn(x64, p.shared.w1.value, p.shared.b1.value, p.shared.w2.value,
+                               p.shared.b2.value)
+    close(got, want, 1e-5)
+
+
+def test_single_expert_equals_dense():
+    # test_arch.py:244-252 / acceptance C8
+    spec = A.LayerSpec(kind="moe", hidden=32, experts=1, gating=GatingConfig(1, 1, 16.0))
+    p = rounded_params(spec, 1, torch.float32)
+    x64 = np.random.default_rng(8).standard_normal((12, 32))
+    got = A.forward_layer(x64, spec, p)
+    dense = A.LayerSpec(kind="dense", hidden=32)
+    want = A.forward_layer(x64, dense, p.experts[0])
+    close(got, want, 1e-6)
+    f = p.experts[0]
+    close(want, x64 + O.forward_ffn(x64, f.w1.value, f.b1.value, f.w2.value, f.b2.value), 1e-5)
+
+
+def test_residual_equals_standard_plus_shared():
+    # test_arch.py:254-265
+    spec_r = A.LayerSpec(kind="moe", hidden=64, experts=4, residual=True,
+                         gating=GatingConfig(4, 2, 4.0))
+    p = rounded_params(spec_r, 23, torch.float32)
+    x64 = np.random.default_rng(9).standard_normal((50, 64))
+    res = A.forward_layer(x64, spec_r, p)
+    spec_s = A.LayerSpec(kind="moe", hidden=64, experts=4, gating=GatingConfig(4, 2, 4.0))
+    std = A.forward_layer(x64, spec_s, A.MoeLayerParams(p.gate_w, p.experts, None))
+    mlp = A.forward_ffn(x64, p.shared)
+    close(res, std + mlp, 1e-5)
+
+
+def test_width_mismatch_rejected():
+    spec = A.LayerSpec(kind="dense", hidden=8)
+    p = A.init_layer_params(spec, np.random.default_rng(0))
+    with pytest.raises(ValueError):
+        A.forward_layer(np.zeros((3, 7)), spec, p)
+
+
+def test_config1_fp32_full():
+    """BASELINE config 1 (S=4096, E=8, M=1024, top-1, cf=1.0, fp32): full output."""
+    spec = A.LayerSpec(kind="moe", hidden=1024, experts=8, gating=GatingConfig(8, 1, 1.0))
+    p = rounded_params(spec, 0, torch.float32)
+    x64 = np.random.default_rng(0).standard_normal((4096, 1024)).astype(np.float32).astype(np.float64)
+    layer, x, out, logits = run_layer(spec, p, x64, torch.float32)
+    lg, _ = check_routing(layer, logits, spec, 4096)
+    ex, sh = oracle_args(p)
+    want = O.forward_layer_with_logits(x64, lg, ex, sh, 8, 1, 1.0)
+    close(out.cpu().numpy(), want, 1e-5)
+
+
+@pytest.mark.parametrize("cfg", [
+    # (S, M, E, k, cf, residual, skew, experts checked)
+    (16384, 1024, 16, 2, 1.25, False, 0.5, [0, 5, 11]),   # BASELINE config 2 (drops)
+    (16384, 1024, 32, 1, 1.0, True, 0.5, [0, 7, 31]),     # config 4, PR-MoE-32 layer
+    (16384, 1024, 64, 1, 1.0, True, 0.0, [1, 40]),        # config 4, PR-MoE-64 layer
+    (2000, 256, 8, 2, 0.7, True, 1.0, list(range(8))),    # ragged S, heavy drops
+])
+def test_bf16_layers_sampled(cfg):
+    S, M, E, k, cf, res, skew, subset = cfg
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=res,
+                       gating=GatingConfig(E, k, cf))
+    p = rounded_params(spec, S + E, torch.bfloat16)
+    rng = np.random.default_rng(E)
+    if skew:
+        # shift the gate toward a few experts so capacity drops happen
+        p.gate_w.value[:] += torch.as_tensor(rng.normal(0, skew, size=(1, E)) / 8).to(
+            torch.bfloat16).double().numpy()
+    x64 = torch.as_tensor(rng.standard_normal((S, M))).to(torch.bfloat16).double().numpy()
+    layer, x, out, logits = run_layer(spec, p, x64, torch.bfloat16)
+    lg, slots = check_routing(layer, logits, spec, S)
+    ex, sh = oracle_args(p)
+    tok, want = O.forward_layer_sampled(x64, lg, ex, sh, E, k, cf, subset)
+    assert tok.size > 0
+    close(out.float().cpu().numpy()[tok], want, 2e-2)
+
+
+def test_config3_routing_full_and_sampled_outputs():
+    """BASELINE config 3 shape on one GPU (S=65536, M=2048, F=8192, E=128, top-1):
+    routing bit-exact on all tokens, outputs checked on 3 experts + dropped tokens."""
+    S, M, E = 65536, 2048, 128
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, 1, 1.0))
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    # device-side init (4.3 G weights would take minutes in NumPy)
+    dev = "cuda"
+    gw = (torch.randn(M, E, device=dev, generator=gen) * 0.1).to(torch.bfloat16)
+    w1 = (torch.randn(E, M, 4 * M, device=dev, generator=gen, dtype=torch.bfloat16) * 0.1)
+    w2 = (torch.randn(E, 4 * M, M, device=dev, generator=gen, dtype=torch.bfloat16) * 0.1)
+    zb1, zb2 = torch.zeros(1, 4 * M, device=dev), torch.zeros(1, M, device=dev)
+    p = A.MoeLayerParams(gate_w=gw, experts=tuple(A.FfnParams(w1[e], zb1, w2[e], zb2)
+                                                   for e in range(E)))
+    layer = A.MoeLayer(spec, p, dtype=torch.bfloat16)
+    x = torch.randn(S, M, device=dev, generator=gen).to(torch.bfloat16)
+    logits = torch.empty(S, E, device=dev)
+    out = layer(x, logits_out=logits)
+    torch.cuda.synchronize()
+    lg, slots = check_routing(layer, logits, spec, S)
+    subset = [0, 63, 127]
+    x64 = x.double().cpu().numpy()
+    ex = []
+    for e in range(E):
+        if e in subset:
+            ex.append((w1[e].double().cpu().numpy(), np.zeros((1, 4 * M)),
+                       w2[e].double().cpu().numpy(), np.zeros((1, M))))
+        else:
+            ex.append(None)
+    tok, want = O.forward_layer_sampled(x64, lg, ex, None, E, 1, 1.0, subset)
+    assert tok.size > 1000
+    close(out[torch.as_tensor(tok, device=dev)].float().cpu().numpy(), want, 2e-2)
+    dropped = (slots < 0).all(axis=1)
+    d = torch.as_tensor(dropped, device=dev)
+    assert torch.equal(out[d], x[d])

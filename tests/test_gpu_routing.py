@@ -1,0 +1,181 @@
+"""GPU parity of the routing kernels against the reference's golden vectors and
+the CPU oracle. Integer outputs (ids, slots, loads, scans) must be bit-exact;
+float64 scatter/combine are bit-exact too (exact copies, individually rounded
+IEEE ops); float64 softmax probabilities agree to a few ulp."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_oracle as O
+from paper_2201_05596_b200 import gating as G
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def _load(name):
+    return np.load(os.path.join(GOLDEN, name))
+
+
+def test_gate_kats_golden():
+    z = _load("gate_kats.npz")
+    for i in range(int(z["n"])):
+        lg, k = z[f"c{i}_logits"], int(z[f"c{i}_k"])
+        g = G.top_k_gate(lg, G.GatingConfig(lg.shape[1], k))
+        assert g.expert_ids.dtype == np.int64
+        assert np.array_equal(g.expert_ids, z[f"c{i}_ids"]), i
+        np.testing.assert_allclose(g.gate_probs, z[f"c{i}_gp"], rtol=1e-14, atol=1e-300)
+        np.testing.assert_allclose(g.probs, z[f"c{i}_probs"], rtol=1e-14, atol=1e-300)
+
+
+def test_gate_literal_kats():
+    # test_gating.py:65-98
+    assert G.top_k_gate(np.array([[1.0, 3.0, 2.0]]), G.GatingConfig(3, 1)).expert_ids.tolist() == [[1]]
+    assert G.top_k_gate(np.array([[5.0, 5.0, 1.0]]), G.GatingConfig(3, 2)).expert_ids.tolist() == [[0, 1]]
+    assert G.top_k_gate(np.array([[2.0, 7.0, 7.0, 7.0]]), G.GatingConfig(4, 1)).expert_ids.tolist() == [[1]]
+    assert G.top_k_gate(np.array([[0.0, -0.0, 1.0, 1.0]]), G.GatingConfig(4, 2)).expert_ids.tolist() == [[2, 3]]
+    g = G.top_k_gate(np.array([[0.4, 2.0, -1.0, 1.5]]), G.GatingConfig(4, 2))
+    assert g.gate_probs[0].sum() < 1.0
+    rng = np.random.default_rng(42)
+    g = G.top_k_gate(rng.standard_normal((50, 8)), G.GatingConfig(8, 2))
+    assert np.allclose(g.probs.sum(axis=1), 1.0, atol=1e-12)
+    assert (g.expert_ids[:, 0] != g.expert_ids[:, 1]).all()
+
+
+def test_gate_shape_errors():
+    with pytest.raises(G.ShapeError if hasattr(G, "ShapeError") else ValueError):
+        G.top_k_gate(np.zeros((4, 5)), G.GatingConfig(8, 1))
+    with pytest.raises(ValueError):
+        G.top_k_gate(np.zeros(5), G.GatingConfig(5, 1))
+
+
+def test_plans_golden_bitwise():
+    z = _load("plans.npz")
+    for i in range(int(z["n"])):
+        e, k, cf = z[f"p{i}_cfg"]
+        cfg = G.GatingConfig(int(e), int(k), float(cf))
+        lg = z[f"p{i}_logits"]
+        gate = G.top_k_gate(lg, cfg)
+        assert np.array_equal(gate.expert_ids, z[f"p{i}_ids"]), i
+        plan = G.build_dispatch_plan(gate, cfg, lg.shape[0])
+        assert plan.capacity == int(z[f"p{i}_cap"])
+        assert plan.slots.dtype == np.int64
+        assert np.array_equal(plan.slots, z[f"p{i}_slots"]), i
+        assert np.array_equal(plan.expert_load, z[f"p{i}_load"]), i
+
+
+@pytest.mark.parametrize("S,E,k,cf,skew", [
+    (65536, 128, 1, 1.0, 0.0), (65536, 128, 1, 1.0, 0.5), (16384, 16, 2, 1.25, 0.5),
+    (4096, 8, 1, 1.0, 0.5), (1000, 3072, 2, 0.3, 1.0), (129, 2, 2, 2.0, 0.0), (1, 4, 1, 1.0, 0.0),
+])
+def test_plan_random_vs_oracle(S, E, k, cf, skew):
+    rng = np.random.default_rng(S + E)
+    lg = (rng.standard_normal((S, E)) + rng.normal(0, skew, size=(1, E))).astype(np.float32)
+    cfg = G.GatingConfig(E, k, cf)
+    dev = torch.from_numpy(lg).cuda()
+    gate = G.top_k_gate(dev, cfg)  # device path: fp32 comparisons
+    ids_ref, gp_ref, _ = O.top_k_gate(lg.astype(np.float64), E, k)
+    assert np.array_equal(gate.expert_ids.cpu().numpy(), ids_ref)
+    np.testing.assert_allclose(gate.gate_probs.cpu().numpy(), gp_ref, rtol=2e-6)
+    plan = G.build_dispatch_plan(gate, cfg, S)
+    slots, load, cap = O.build_dispatch_plan_fast(ids_ref, E, k, cf)
+    assert plan.capacity == cap
+    assert np.array_equal(plan.slots.cpu().numpy(), slots)
+    assert np.array_equal(plan.expert_load.cpu().numpy(), load)
+
+
+def test_plan_determinism_and_empty():
+    rng = np.random.default_rng(6)
+    lg = rng.standard_normal((40, 4))
+    cfg = G.GatingConfig(4, 2, 1.0)
+    a = G.build_dispatch_plan(G.top_k_gate(lg, cfg), cfg, 40)
+    b = G.build_dispatch_plan(G.top_k_gate(lg.copy(), cfg), cfg, 40)
+    assert np.array_equal(a.slots, b.slots) and np.array_equal(a.gate_probs, b.gate_probs)
+    cfg = G.GatingConfig(4, 1)
+    plan = G.build_dispatch_plan(G.top_k_gate(np.zeros((0, 4)), cfg), cfg, 0)
+    assert plan.capacity == 0 and plan.slots.shape == (0, 1)
+    c = G.OpCounter()
+    buf = G.scatter_tokens(np.zeros((0, 3)), plan, c)
+    assert buf.data.shape == (4, 0, 3)
+    assert G.combine_tokens(buf, plan, c).shape == (0, 3) and c.ops == 0
+
+
+def test_scans_golden_bitwise():
+    z = _load("scans.npz")
+    assert G.exclusive_scan_blelloch(z["worked_in"]).tolist() == [0, 3, 4, 11, 11, 15, 16, 22]
+    for i in range(int(z["n_int"])):
+        got = G.exclusive_scan_blelloch(z[f"i{i}_in"])
+        assert got.dtype == np.int64 and np.array_equal(got, z[f"i{i}_out"]), i
+    for i in range(int(z["n_float"])):
+        assert np.array_equal(G.exclusive_scan_blelloch(z[f"f{i}_in"]), z[f"f{i}_out"]), i
+    with pytest.raises(ValueError):
+        G.exclusive_scan_blelloch(np.zeros((2, 2)))
+    assert G.exclusive_scan_blelloch(np.array([], dtype=np.int64)).shape == (0,)
+
+
+def test_scan_long_vectors():
+    # acceptance C5 (test_acceptance.py:168-187) plus a multi-level case
+    rng = np.random.default_rng(5)
+    for n in list(range(0, 300)) + [4095, 4096, 4097, 50001, 5_000_001]:
+        v = rng.integers(0, 100, size=n)
+        want = np.concatenate([[0], np.cumsum(v)[:-1]]) if n else np.zeros(0, np.int64)
+        assert np.array_equal(G.exclusive_scan_blelloch(v), want), n
+
+
+def test_scatter_combine_golden_bitwise():
+    z = _load("scatter_combine.npz")
+    for i in range(int(z["n"])):
+        e, k, cf = z[f"s{i}_cfg"]
+        e, k = int(e), int(k)
+        cap = z[f"s{i}_data"].shape[1]
+        s = z[f"s{i}_x"].shape[0]
+        plan = G.DispatchPlan(num_tokens=s, num_experts=e, k=k, capacity=cap,
+                              expert_ids=z[f"s{i}_ids"], gate_probs=z[f"s{i}_gp"],
+                              slots=z[f"s{i}_slots"], expert_load=None)
+        c = G.OpCounter()
+        buf = G.scatter_tokens(z[f"s{i}_x"], plan, c)
+        assert np.array_equal(buf.data, z[f"s{i}_data"]), i
+        assert np.array_equal(buf.occupied, z[f"s{i}_occ"]), i
+
+        class B:
+            data = np.tanh(buf.data)
+        comb = G.combine_tokens(B, plan, c)
+        assert np.array_equal(comb, z[f"s{i}_comb"]), i
+        assert c.ops == int(z[f"s{i}_ops"])
+
+
+def test_scatter_combine_semantics():
+    # test_gating.py:310-348
+    rng = np.random.default_rng(10)
+    cfg = G.GatingConfig(4, 1, 4.0)
+    batch = rng.standard_normal((16, 5))
+    gates = G.top_k_gate(rng.standard_normal((16, 4)), cfg)
+    plan = G.build_dispatch_plan(gates, cfg, 16)
+    out = G.combine_tokens(G.scatter_tokens(batch, plan), plan)
+    assert np.max(np.abs(out - batch * gates.gate_probs[:, 0:1])) <= 1e-15
+    cfg = G.GatingConfig(2, 1, 0.5)
+    plan = G.build_dispatch_plan(G.top_k_gate(np.tile([[1.0, 0.0]], (8, 1)), cfg), cfg, 8)
+    out = G.combine_tokens(G.scatter_tokens(np.ones((8, 3)), plan), plan)
+    assert plan.capacity == 2 and not np.any(out[2:]) and np.all(out[:2] != 0)
+    cfg = G.GatingConfig(1, 1, 1.0)
+    batch = rng.standard_normal((10, 4))
+    plan = G.build_dispatch_plan(G.top_k_gate(np.zeros((10, 1)), cfg), cfg, 10)
+    assert np.array_equal(G.combine_tokens(G.scatter_tokens(batch, plan), plan), batch)
+
+
+def test_device_tensors_stay_on_device():
+    cfg = G.GatingConfig(16, 2, 1.25)
+    x = torch.randn(1000, 64, device="cuda", dtype=torch.bfloat16)
+    lg = torch.randn(1000, 16, device="cuda")
+    gate = G.top_k_gate(lg, cfg)
+    plan = G.build_dispatch_plan(gate, cfg, 1000)
+    buf = G.scatter_tokens(x, plan)
+    assert buf.data.is_cuda and buf.data.dtype == torch.bfloat16
+    out = G.combine_tokens(buf, plan)
+    # identity experts: out = x * (p0 [+ p1]) over kept choices
+    kept = (plan.slots >= 0).float()
+    w = (gate.gate_probs * kept).sum(1, keepdim=True)
+    torch.testing.assert_close(out.float(), x.float() * w, rtol=1e-2, atol=1e-2)
