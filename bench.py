@@ -1,0 +1,317 @@
+"""MoE-layer forward benchmark (BASELINE.json metric: tokens/s at the
+1.3B+MoE-128 layer shape on 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A step is one full MoE-layer forward (gate GEMM + routing epilogue, capacity
+scan, dispatch, grouped expert GEMM1/GEMM2, combine + residual) over one batch
+of synthetic tokens already resident in HBM. N=1 runs BASELINE config 3 on one
+GPU (S=65536, d_model=2048, d_ff=8192, 128 experts, top-1, cf=1.0, bf16).
+N>1 (torchrun, one rank per GPU, NCCL) runs the expert-parallel layer with
+S=65536 tokens per rank (weak scaling: global batch 65536*N, global capacity).
+
+``--impl reference`` times the reference algorithm on the host CPU: the CPU
+oracle (oracle/moe_oracle.py, a float64 NumPy restatement of moekit's
+forward_layer) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer fwd tokens/s @1.3B+MoE-128 shape"
+UNIT = "tokens/s"
+C3 = dict(S=65536, M=2048, E=128, k=1, cf=1.0)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--tokens", type=int, default=C3["S"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of moekit.arch.forward_layer)
+# ---------------------------------------------------------------------------
+
+CPU_SAMPLE = dict(S=4096, M=2048, E=8, k=1, cf=1.0)  # 8 experts x cap 512 of the C3 expert shape
+
+
+def cpu_reference_step(state=None):
+    from oracle import moe_oracle as O
+
+    if state is None:
+        s = CPU_SAMPLE
+        rng = np.random.default_rng(0)
+        gw, experts, _ = O.init_layer_params(s["M"], s["E"], False, rng)
+        x = rng.standard_normal((s["S"], s["M"]))
+        state = (x, gw, experts)
+    x, gw, experts = state
+    t0 = time.perf_counter()
+    O.forward_layer(x, gw, experts, None, CPU_SAMPLE["E"], CPU_SAMPLE["k"], CPU_SAMPLE["cf"])
+    return time.perf_counter() - t0, state
+
+
+def cpu_desc():
+    s = CPU_SAMPLE
+    return (f"oracle forward_layer (float64 NumPy/OpenBLAS) on {s['S']} tokens x {s['E']} experts "
+            f"of the C3 expert shape (d_model {s['M']}, d_ff {4 * s['M']}, top-1, cf 1.0 -> "
+            f"capacity 512 = the C3 per-expert load)")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    times, state = [], None
+    for i in range(args.warmup + args.steps):
+        dt, state = cpu_reference_step(state)
+        if i >= args.warmup:
+            times.append(dt)
+    med = statistics.median(times)
+    value = CPU_SAMPLE["S"] / med
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C3 expert shape, CPU-bounded sample", **CPU_SAMPLE},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": cpu_desc()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        self.idx = gpu_index
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        mx = max(r[1] for r in rows)
+        loaded = [r for r in rows if r[0] > 0.5 * mx] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[2]) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        p = json.load(open(path))
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def make_layer(S, M, E, k, cf, dev, seed=0):
+    import torch
+
+    from paper_2201_05596_b200 import arch as A
+    from paper_2201_05596_b200.gating import GatingConfig
+
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, k, cf))
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    F = 4 * M
+    # random-init weights of the named architecture: N(0,1)*0.1, zero biases (arch.py:347-365)
+    gw = torch.randn(M, E, device=dev, generator=gen) * 0.1
+    w1 = torch.randn(E, M, F, device=dev, generator=gen, dtype=torch.bfloat16) * 0.1
+    w2 = torch.randn(E, F, M, device=dev, generator=gen, dtype=torch.bfloat16) * 0.1
+    zb1, zb2 = torch.zeros(1, F, device=dev), torch.zeros(1, M, device=dev)
+    p = A.MoeLayerParams(gate_w=gw, experts=tuple(A.FfnParams(w1[e], zb1, w2[e], zb2)
+                                                   for e in range(E)))
+    layer = A.MoeLayer(spec, p, dtype=torch.bfloat16, device=dev)
+    del w1, w2, p
+    torch.cuda.empty_cache()
+    return layer
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2201_05596_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    S, M, E, k, cf = args.tokens, C3["M"], C3["E"], C3["k"], C3["cf"]
+    F = 4 * M
+    if world > 1:
+        from paper_2201_05596_b200.ep import EPMoeLayer
+
+        layer = EPMoeLayer.synthetic(S, M, E, k, cf, dev, seed=0)
+    else:
+        layer = make_layer(S, M, E, k, cf, dev)
+    gen = torch.Generator(device=dev).manual_seed(1 + rank)
+    x = torch.randn(S, M, device=dev, generator=gen).to(torch.bfloat16)
+    # drop-free synthetic routing at C3 with unbiased logits is ~1.9% drops
+    out = torch.empty_like(x)
+    for _ in range(args.warmup):
+        layer(x, out=out)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K full forwards, inputs resident (x 268 MB + weights 8.6 GB >> L2)
+    timer = _lib.PhaseTimer()
+    launches0 = _lib.launch_count()
+    clocks = Clocks(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        layer(x, out=out, timer=timer)
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    phases = timer.summary(args.steps)
+    kept = int(layer.kept_assignments(S)) if hasattr(layer, "kept_assignments") else S * k
+    # ---- e2e through the public API: pinned host x -> layer -> host out
+    xh = x.cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    for _ in range(2):
+        oh.copy_(layer(xh), non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        oh.copy_(layer(xh), non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+        kt = torch.tensor([kept], device=dev, dtype=torch.int64)
+        dist.all_reduce(kt)
+        kept_total = int(kt.item())
+    else:
+        kept_total = kept
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    hbm, tf_burst, tf_sus, src = peaks()
+    # dominant kernel: the grouped expert GEMM (GEMM1 + GEMM2 launches)
+    gemm_ms = phases.get("gemm1", 0.0) + phases.get("gemm2", 0.0)
+    kept_rank = kept_total / world
+    flops = 4.0 * kept_rank * M * F  # 2*A*M*F per GEMM launch, two launches
+    achieved = flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("grouped_gemm_bytes_per_step")
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        dt, _ = cpu_reference_step()
+        cpu = {"value": CPU_SAMPLE["S"] / dt, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
+               "kind": "port", "sample": cpu_desc()}
+    value = S * world / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "C3: 1.3B+MoE-128 MoE layer (d_model 2048, d_ff 8192, 128 experts,"
+                               " top-1, cf 1.0)", "tokens_per_gpu": S, "global_batch": S * world,
+                   "parallelism": f"ep{world}" if world > 1 else "single", "l2": "inputs larger "
+                   "than L2 (x 268 MB, expert weights 8.6 GB per layer)"},
+        "roofline": {"bound": "tensor", "kernel": "grouped expert GEMM (GEMM1+GEMM2)",
+                     "achieved": achieved, "peak": tf_sus, "unit": "TFLOP/s",
+                     "frac": achieved / tf_sus if achieved else None, "traffic": traffic,
+                     "peak_kind": f"{src} sustained (burst {tf_burst})",
+                     "frac_of_burst": achieved / tf_burst if achieved else None},
+        "phases_ms": phases,
+        "kept_assignments_per_gpu": kept_rank,
+        "cpu_baseline": cpu,
+        "e2e": {"value": S * world / (e2e_ms * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": S * M * 2, "d2h_bytes_per_step": S * M * 2},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

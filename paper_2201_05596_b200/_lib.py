@@ -105,6 +105,7 @@ def check(rc: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     lib = load()
+    _count(name)
     check(getattr(lib, name)(*args), name)
 
 
@@ -116,3 +117,48 @@ def dtype_code(dt: torch.dtype) -> int:
     if dt == torch.float64:
         return MOE_F64
     raise TypeError(f"unsupported dtype {dt}")
+
+
+# ---------------------------------------------------------------------------
+# instrumentation: kernel-launch counter and per-phase CUDA-event timer
+# ---------------------------------------------------------------------------
+
+_NON_LAUNCH = {"moe_abi_version", "moe_plan_workspace_bytes", "moe_scan_workspace_bytes"}
+# entry points that launch more than one kernel per call
+_MULTI = {"moe_build_plan": 3}
+_launches = 0
+
+
+def launch_count() -> int:
+    """Number of kernel launches issued through this binding (per process)."""
+    return _launches
+
+
+def _count(name: str) -> None:
+    global _launches
+    if name not in _NON_LAUNCH:
+        _launches += _MULTI.get(name, 1)
+
+
+class PhaseTimer:
+    """CUDA events around named phases on the current stream; no host sync
+    inside the timed region (events are read after the caller synchronizes)."""
+
+    def __init__(self) -> None:
+        self.rec: list[tuple[str, torch.cuda.Event, torch.cuda.Event]] = []
+
+    def start(self, name: str):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        return (name, e0)
+
+    def stop(self, tok) -> None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self.rec.append((tok[0], tok[1], e1))
+
+    def summary(self, steps: int) -> dict:
+        out: dict[str, float] = {}
+        for name, a, b in self.rec:
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return {k: v / max(steps, 1) for k, v in out.items()}

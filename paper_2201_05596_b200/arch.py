@@ -176,6 +176,20 @@ class DenseFfn:
         return out
 
 
+class _Phases:
+    """Optional per-phase CUDA-event timing (bench.py); a no-op without a timer."""
+
+    def __init__(self, timer) -> None:
+        self.timer, self.tok = timer, None
+
+    def __call__(self, name) -> None:
+        if self.timer is None:
+            return
+        if self.tok is not None:
+            self.timer.stop(self.tok)
+        self.tok = self.timer.start(name) if name else None
+
+
 def _grouped_gemm(dtype, a, a_rows, K, w, N, bias, d, G, row_start, row_stride, rows, rows_const,
                   max_rows, act):
     st = _lib.stream_ptr()
@@ -272,18 +286,20 @@ class MoeLayer:
 
     # -- forward ---------------------------------------------------------------
     def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None,
-                 logits_out: torch.Tensor | None = None) -> torch.Tensor:
-        return self.forward(x, out, logits_out)
+                 logits_out: torch.Tensor | None = None, timer=None) -> torch.Tensor:
+        return self.forward(x, out, logits_out, timer)
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None,
-                logits_out: torch.Tensor | None = None) -> torch.Tensor:
+                logits_out: torch.Tensor | None = None, timer=None) -> torch.Tensor:
         """out = x + combine(experts(dispatch(x))) [+ shared MLP(x)]
         (arch.py:372-392). ``logits_out`` (S, E) fp32 receives the gate logits
         the routing decided on (the parity tests feed them to the oracle)."""
         if x.dim() != 2 or x.shape[1] != self.M:
             raise ShapeError(f"batch width {tuple(x.shape)} does not match layer hidden {self.M}")
-        if x.dtype != self.dtype or x.device != self.device:
-            x = x.to(device=self.device, dtype=self.dtype)
+        if x.device != self.device:  # host input: one H2D copy on the current stream
+            x = x.to(device=self.device, non_blocking=True)
+        if x.dtype != self.dtype:
+            x = x.to(self.dtype)
         x = x.contiguous()
         S = x.shape[0]
         out = torch.empty_like(x) if out is None else out
@@ -293,6 +309,8 @@ class MoeLayer:
         cap, E, M, F, k = ws["cap"], self.E, self.M, self.F, self.k
         st = _lib.stream_ptr()
         ids, gp, lr, tc = ws["ids"], ws["gp"], ws["local_rank"], ws["tile_counts"]
+        ph = _Phases(timer)
+        ph("gate")
         if self.dtype == torch.bfloat16:
             _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k,
                       _lib.ptr(logits_out), ids.data_ptr(), gp.data_ptr(), lr.data_ptr(),
@@ -304,24 +322,34 @@ class MoeLayer:
             _lib.call("moe_topk_gate", logits.data_ptr(), _lib.MOE_F32, S, E, k, ids.data_ptr(),
                       gp.data_ptr(), None, st)
             _lib.call("moe_plan_tiles", ids.data_ptr(), S, E, k, lr.data_ptr(), tc.data_ptr(), st)
+        ph("scan")
         _lib.call("moe_plan_scan", tc.data_ptr(), S, E, cap, None, ws["tile_offsets"].data_ptr(),
                   ws["totals"].data_ptr(), ws["load"].data_ptr(), st)
+        ph("dispatch")
         _lib.call("moe_dispatch", x.data_ptr(), S, M * x.element_size(), E, k, cap, ids.data_ptr(),
                   lr.data_ptr(), ws["tile_offsets"].data_ptr(), ws["slots"].data_ptr(),
                   ws["xbuf"].data_ptr(), st)
         if cap > 0:
+            ph("gemm1")
             _grouped_gemm(self.dtype, ws["xbuf"], E * cap, M, self.w1, F, self.b1, ws["h"], E,
                           None, cap, ws["load"], 0, cap, _lib.MOE_ACT_GELU)
+            ph("gemm2")
             _grouped_gemm(self.dtype, ws["h"], E * cap, F, self.w2, M, self.b2, ws["y"], E, None,
                           cap, ws["load"], 0, cap, _lib.MOE_ACT_NONE)
         shared_out = None
         if self.shared is not None:
+            ph("shared_mlp")
             shared_out = self.shared(x, ws["hs"], ws["ys"])
-        gp_code = _lib.MOE_F32
+        ph("combine")
         _lib.call("moe_combine", ws["y"].data_ptr(), _lib.dtype_code(self.dtype), S, M, E, k, cap,
-                  ids.data_ptr(), ws["slots"].data_ptr(), None, gp.data_ptr(), gp_code,
+                  ids.data_ptr(), ws["slots"].data_ptr(), None, gp.data_ptr(), _lib.MOE_F32,
                   x.data_ptr(), _lib.ptr(shared_out), out.data_ptr(), 1, st)
+        ph(None)
         return out
+
+    def kept_assignments(self, S: int) -> int:
+        """Kept (non-dropped) assignments of the last forward of size S (host sync)."""
+        return int(self._ws[S]["load"].sum().item())
 
     def plan(self, S: int):
         """(ids, gate_probs, slots, expert_load, capacity) of the last forward of size S."""

@@ -241,22 +241,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (EPI != EPI_GATE) {
         const float* bias = args.bias ? args.bias + (int64_t)w * N : nullptr;
         const bool vec_ok = (N % 8) == 0;
-#pragma unroll 1
+        __nv_bfloat16* drow = args.D + out_row * N;
+        // TMEM loads double-buffered across 32-column chunks: the load of
+        // chunk c+1 is in flight while chunk c is biased, activated and stored.
+        uint32_t r[2][32];
+        tmem_ld_32x32b_x32(t_addr, r[0]);
+#pragma unroll
         for (int c = 0; c < BN / 32; ++c) {
           const int col0 = nb * BN + c * 32;
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_addr + c * 32, r);
-          tmem_ld_wait();
+          float bv[32];
+          if (bias != nullptr && vec_ok && col0 + 32 <= N) {
+            const float4* b4 = reinterpret_cast<const float4*>(bias + col0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 t4 = __ldg(b4 + q);
+              bv[4 * q] = t4.x; bv[4 * q + 1] = t4.y; bv[4 * q + 2] = t4.z; bv[4 * q + 3] = t4.w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              bv[i] = (bias != nullptr && col0 + i < N) ? __ldg(bias + col0 + i) : 0.f;
+          }
+          tmem_ld_wait_regs(r[c & 1]);
+          if (c + 1 < BN / 32) tmem_ld_32x32b_x32(t_addr + (c + 1) * 32, r[(c + 1) & 1]);
           if (!valid || col0 >= N) continue;
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            v[i] = __uint_as_float(r[i]);
-            const int col = col0 + i;
-            if (bias != nullptr && col < N) v[i] += __ldg(bias + col);
+            v[i] = __uint_as_float(r[c & 1][i]) + bv[i];
             if constexpr (EPI == EPI_BIAS_GELU) v[i] = gelu_tanh_fast(v[i]);
           }
-          __nv_bfloat16* drow = args.D + out_row * N;
           if (vec_ok && col0 + 32 <= N) {
             uint4* dst = reinterpret_cast<uint4*>(drow + col0);
 #pragma unroll
@@ -274,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (col0 + i < N) drow[col0 + i] = __float2bfloat16_rn(v[i]);
           }
         }
+        tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);

@@ -278,7 +278,7 @@ __global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t S, int64_t
   const int64_t nvec = row_bytes / (int64_t)sizeof(V);
   for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
        t += warps_total) {
-    int64_t dst_row[2] = {-1, -1};
+    int64_t dst0 = -1, dst1 = -1;
     for (int j = 0; j < k; ++j) {
       const int e = ids[t * k + j];
       int64_t slot;
@@ -290,14 +290,15 @@ __global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t S, int64_t
         slot = slots[t * k + j];
       }
       if (slot >= 0) {
-        dst_row[j] = (int64_t)e * cap + slot;
-        if (occupied != nullptr && lane == 0) occupied[dst_row[j]] = 1;
+        const int64_t d = (int64_t)e * cap + slot;
+        if (j == 0) dst0 = d; else dst1 = d;
+        if (occupied != nullptr && lane == 0) occupied[d] = 1;
       }
     }
-    if (dst_row[0] < 0 && dst_row[1] < 0) continue;
+    if (dst0 < 0 && dst1 < 0) continue;
     const V* src = reinterpret_cast<const V*>(x + t * row_bytes);
-    V* d0 = dst_row[0] >= 0 ? reinterpret_cast<V*>(buf + dst_row[0] * row_bytes) : nullptr;
-    V* d1 = dst_row[1] >= 0 ? reinterpret_cast<V*>(buf + dst_row[1] * row_bytes) : nullptr;
+    V* d0 = dst0 >= 0 ? reinterpret_cast<V*>(buf + dst0 * row_bytes) : nullptr;
+    V* d1 = dst1 >= 0 ? reinterpret_cast<V*>(buf + dst1 * row_bytes) : nullptr;
     constexpr int U = 4;
     int64_t i = lane;
     for (; i + 32 * (U - 1) < nvec; i += 32 * U) {
@@ -352,21 +353,28 @@ MOE_DEV double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 // kExpertOrder: contributions summed in ascending expert id (forward_layer's
 // loop over experts); otherwise in choice order (combine_tokens' np.add.at).
 // Every multiply/add is individually rounded so f64 results match NumPy.
-template <typename T, typename P, bool kExpertOrder>
+// Warp per token; each lane moves VEC elements (16 B) per access.
+template <typename T, int VEC>
+struct alignas(sizeof(T) * VEC) Pack {
+  T v[VEC];
+};
+
+template <typename T, typename P, bool kExpertOrder, int VEC>
 __global__ void combine_kernel(const T* __restrict__ y, int64_t S, int M, int k, int E, int64_t cap,
                                const int32_t* __restrict__ ids, const int32_t* __restrict__ slots,
                                const int32_t* __restrict__ row_index, const P* __restrict__ gp,
                                const T* __restrict__ x, const T* __restrict__ shared,
                                T* __restrict__ out) {
   using A = typename Acc<T>::type;
+  using V = Pack<T, VEC>;
   const int lane = threadIdx.x & 31;
   const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int nv = M / VEC;
   for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
        t += warps_total) {
-    int64_t row[2] = {-1, -1};
-    A p[2] = {0, 0};
-    int ex[2] = {0, 0};
-    int n = 0;
+    int64_t r0 = -1, r1 = -1;
+    A p0 = 0, p1 = 0;
+    int e0 = 0, e1 = 0, n = 0;
     for (int j = 0; j < k; ++j) {
       int64_t r;
       if (row_index != nullptr) {
@@ -376,27 +384,45 @@ __global__ void combine_kernel(const T* __restrict__ y, int64_t S, int M, int k,
         r = s >= 0 ? (int64_t)ids[t * k + j] * cap + s : -1;
       }
       if (r >= 0) {
-        row[n] = r;
-        p[n] = (A)gp[t * k + j];
-        ex[n] = ids[t * k + j];
+        const A pj = (A)gp[t * k + j];
+        const int ej = ids[t * k + j];
+        if (n == 0) { r0 = r; p0 = pj; e0 = ej; }
+        else { r1 = r; p1 = pj; e1 = ej; }
         ++n;
       }
     }
-    if (kExpertOrder && n == 2 && ex[1] < ex[0]) {
-      int64_t tr = row[0]; row[0] = row[1]; row[1] = tr;
-      A tp = p[0]; p[0] = p[1]; p[1] = tp;
+    if (kExpertOrder && n == 2 && e1 < e0) {
+      int64_t tr = r0; r0 = r1; r1 = tr;
+      A tp = p0; p0 = p1; p1 = tp;
     }
-    for (int c = lane; c < M; c += 32) {
-      A acc = 0;  // the zero accumulator of scatter_rows / np.add.at
-      for (int i = 0; i < n; ++i) acc = add_rn(acc, mul_rn(p[i], to_acc(y[row[i] * M + c])));
-      A o = acc;
-      if (x != nullptr) o = add_rn(to_acc(x[t * M + c]), acc);
-      if (shared != nullptr) o = add_rn(o, to_acc(shared[t * M + c]));
-      if constexpr (sizeof(T) == 8) {
-        out[t * M + c] = o;
-      } else {
-        out[t * M + c] = from_acc<T>(o);
+    const V* y0 = reinterpret_cast<const V*>(y + (n > 0 ? r0 : 0) * M);
+    const V* y1 = reinterpret_cast<const V*>(y + (n > 1 ? r1 : 0) * M);
+    const V* xv = reinterpret_cast<const V*>(x + t * M);
+    const V* sv = reinterpret_cast<const V*>(shared + t * M);
+    V* ov = reinterpret_cast<V*>(out + t * M);
+#pragma unroll 4
+    for (int c = lane; c < nv; c += 32) {
+      V a0, a1, xa, sa;
+      if (n > 0) a0 = y0[c];
+      if (n > 1) a1 = y1[c];
+      if (x != nullptr) xa = xv[c];
+      if (shared != nullptr) sa = sv[c];
+      V o;
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        A acc = 0;  // the zero accumulator of scatter_rows / np.add.at
+        if (n > 0) acc = add_rn(acc, mul_rn(p0, to_acc(a0.v[i])));
+        if (n > 1) acc = add_rn(acc, mul_rn(p1, to_acc(a1.v[i])));
+        A r = acc;
+        if (x != nullptr) r = add_rn(to_acc(xa.v[i]), acc);
+        if (shared != nullptr) r = add_rn(r, to_acc(sa.v[i]));
+        if constexpr (sizeof(T) == 8) {
+          o.v[i] = r;
+        } else {
+          o.v[i] = from_acc<T>(r);
+        }
       }
+      ov[c] = o;
     }
   }
 }
@@ -510,19 +536,36 @@ int launch_scatter(const void* x, int64_t S, int64_t row_bytes, int k, int E, in
   return (int)cudaGetLastError();
 }
 
+template <typename T, typename P, int VEC>
+static void combine_vec(bool expert_order, int g, int threads, cudaStream_t st, const void* y,
+                        int64_t S, int M, int k, int E, int64_t cap, const int32_t* ids,
+                        const int32_t* slots, const int32_t* row_index, const void* gp,
+                        const void* x, const void* shared, void* out) {
+  if (expert_order)
+    combine_kernel<T, P, true, VEC><<<g, threads, 0, st>>>(
+        (const T*)y, S, M, k, E, cap, ids, slots, row_index, (const P*)gp, (const T*)x,
+        (const T*)shared, (T*)out);
+  else
+    combine_kernel<T, P, false, VEC><<<g, threads, 0, st>>>(
+        (const T*)y, S, M, k, E, cap, ids, slots, row_index, (const P*)gp, (const T*)x,
+        (const T*)shared, (T*)out);
+}
+
 template <typename T, typename P>
 static void combine_dispatch(bool expert_order, int g, int threads, cudaStream_t st, const void* y,
                              int64_t S, int M, int k, int E, int64_t cap, const int32_t* ids,
                              const int32_t* slots, const int32_t* row_index, const void* gp,
                              const void* x, const void* shared, void* out) {
-  if (expert_order)
-    combine_kernel<T, P, true><<<g, threads, 0, st>>>((const T*)y, S, M, k, E, cap, ids, slots,
-                                                      row_index, (const P*)gp, (const T*)x,
-                                                      (const T*)shared, (T*)out);
+  constexpr int VEC = 16 / sizeof(T);
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
+  const bool vec_ok = (M % VEC) == 0 && aligned(out) && (y == nullptr || aligned(y)) &&
+                      (x == nullptr || aligned(x)) && (shared == nullptr || aligned(shared));
+  if (vec_ok)
+    combine_vec<T, P, VEC>(expert_order, g, threads, st, y, S, M, k, E, cap, ids, slots, row_index,
+                           gp, x, shared, out);
   else
-    combine_kernel<T, P, false><<<g, threads, 0, st>>>((const T*)y, S, M, k, E, cap, ids, slots,
-                                                       row_index, (const P*)gp, (const T*)x,
-                                                       (const T*)shared, (T*)out);
+    combine_vec<T, P, 1>(expert_order, g, threads, st, y, S, M, k, E, cap, ids, slots, row_index,
+                         gp, x, shared, out);
 }
 
 int launch_combine(const void* y, int dtype, int64_t S, int M, int k, int E, int64_t cap,
