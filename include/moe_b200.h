@@ -95,6 +95,16 @@ int moe_dispatch(const void* x, int64_t S, int64_t row_bytes, int E, int k, int6
                  const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
                  int32_t* slots, void* buf, void* stream);
 
+/* Expert-parallel dispatch into the all-to-all send buffer. tile_offsets come
+ * from moe_plan_scan with rank_base = slot_base (global slots); a kept
+ * assignment (slot < cap) goes to send row row_base[e] + slot - slot_base[e]
+ * (rows grouped by owner rank, then expert, then slot); row_index (S, k)
+ * receives that row or -1, for the combine after the return all-to-all. */
+int moe_dispatch_ep(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                    const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                    const int32_t* slot_base, const int32_t* row_base, int32_t* slots,
+                    int32_t* row_index, void* send_buf, void* stream);
+
 /* gating.combine_tokens (gating.py:281-307) and the combine + residual of
  * arch.forward_layer (arch.py:389-391, :395-413):
  *   out[t] = ((x_resid[t]) + sum_j gate_prob[t,j] * y[row(t,j)]) + shared_out[t]

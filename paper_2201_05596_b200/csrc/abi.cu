@@ -100,7 +100,7 @@ int moe_scatter(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64
   if (S == 0 || cap == 0) return MOE_OK;
   CHECK(x && ids && slots && buf);
   return moe::launch_scatter(x, S, row_bytes, k, E, cap, ids, const_cast<int32_t*>(slots), nullptr,
-                             nullptr, buf, occupied, S_(stream));
+                             nullptr, buf, occupied, nullptr, nullptr, nullptr, S_(stream));
 }
 
 int moe_dispatch(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
@@ -111,7 +111,19 @@ int moe_dispatch(const void* x, int64_t S, int64_t row_bytes, int E, int k, int6
   if (S == 0) return MOE_OK;
   CHECK(x && ids && local_rank && tile_offsets && slots && (buf || cap == 0));
   return moe::launch_scatter(x, S, row_bytes, k, E, cap, ids, slots, local_rank, tile_offsets, buf,
-                             nullptr, S_(stream));
+                             nullptr, nullptr, nullptr, nullptr, S_(stream));
+}
+
+int moe_dispatch_ep(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                    const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                    const int32_t* slot_base, const int32_t* row_base, int32_t* slots,
+                    int32_t* row_index, void* send_buf, void* stream) {
+  CHECK(S >= 0 && row_bytes >= 0 && row_bytes % 2 == 0 && E >= 1 && (k == 1 || k == 2) &&
+        cap >= 0);
+  if (S == 0) return MOE_OK;
+  CHECK(x && ids && local_rank && tile_offsets && slot_base && row_base && slots && row_index);
+  return moe::launch_scatter(x, S, row_bytes, k, E, cap, ids, slots, local_rank, tile_offsets,
+                             send_buf, nullptr, slot_base, row_base, row_index, S_(stream));
 }
 
 int moe_combine(const void* y, int dtype, int64_t S, int M, int E, int k, int64_t cap,

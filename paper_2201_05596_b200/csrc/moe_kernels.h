@@ -22,7 +22,9 @@ int launch_blelloch_f64(double* tree, int64_t m, cudaStream_t st);
 
 int launch_scatter(const void* x, int64_t S, int64_t row_bytes, int k, int E, int64_t cap,
                    const int32_t* ids, int32_t* slots, const int32_t* local_rank,
-                   const int32_t* tile_offsets, void* buf, uint8_t* occupied, cudaStream_t st);
+                   const int32_t* tile_offsets, void* buf, uint8_t* occupied,
+                   const int32_t* slot_base, const int32_t* row_base, int32_t* row_index,
+                   cudaStream_t st);
 
 int launch_combine(const void* y, int dtype, int64_t S, int M, int k, int E, int64_t cap,
                    const int32_t* ids, const int32_t* slots, const int32_t* row_index,

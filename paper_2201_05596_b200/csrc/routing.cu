@@ -272,7 +272,9 @@ __global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t S, int64_t
                                int E, int64_t cap, const int32_t* __restrict__ ids,
                                int32_t* __restrict__ slots, const int32_t* __restrict__ local_rank,
                                const int32_t* __restrict__ tile_offsets, uint8_t* __restrict__ buf,
-                               uint8_t* __restrict__ occupied) {
+                               uint8_t* __restrict__ occupied, const int32_t* __restrict__ slot_base,
+                               const int32_t* __restrict__ row_base,
+                               int32_t* __restrict__ row_index) {
   const int lane = threadIdx.x & 31;
   const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t nvec = row_bytes / (int64_t)sizeof(V);
@@ -289,11 +291,15 @@ __global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t S, int64_t
       } else {
         slot = slots[t * k + j];
       }
+      int64_t d = -1;
       if (slot >= 0) {
-        const int64_t d = (int64_t)e * cap + slot;
+        // expert-buffer row e*cap + slot, or (EP send buffer) row_base[e] + slot - slot_base[e]
+        d = row_base != nullptr ? (int64_t)row_base[e] + slot - (slot_base ? slot_base[e] : 0)
+                                : (int64_t)e * cap + slot;
         if (j == 0) dst0 = d; else dst1 = d;
         if (occupied != nullptr && lane == 0) occupied[d] = 1;
       }
+      if (row_index != nullptr && lane == 0) row_index[t * k + j] = (int32_t)d;
     }
     if (dst0 < 0 && dst1 < 0) continue;
     const V* src = reinterpret_cast<const V*>(x + t * row_bytes);
@@ -515,24 +521,27 @@ int launch_blelloch_f64(double* tree, int64_t m, cudaStream_t st) {
 
 int launch_scatter(const void* x, int64_t S, int64_t row_bytes, int k, int E, int64_t cap,
                    const int32_t* ids, int32_t* slots, const int32_t* local_rank,
-                   const int32_t* tile_offsets, void* buf, uint8_t* occupied, cudaStream_t st) {
+                   const int32_t* tile_offsets, void* buf, uint8_t* occupied,
+                   const int32_t* slot_base, const int32_t* row_base, int32_t* row_index,
+                   cudaStream_t st) {
   if (S == 0) return 0;
   const int threads = 256;
   const int g = grid_for(S, threads / 32, 148 * 64);
   const uint8_t* xb = (const uint8_t*)x;
   uint8_t* bb = (uint8_t*)buf;
+#define MOE_SCATTER(V)                                                                        \
+  scatter_kernel<V><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots, local_rank, \
+                                           tile_offsets, bb, occupied, slot_base, row_base,     \
+                                           row_index)
   if (row_bytes % 16 == 0)
-    scatter_kernel<uint4><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots,
-                                                 local_rank, tile_offsets, bb, occupied);
+    MOE_SCATTER(uint4);
   else if (row_bytes % 8 == 0)
-    scatter_kernel<uint2><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots,
-                                                 local_rank, tile_offsets, bb, occupied);
+    MOE_SCATTER(uint2);
   else if (row_bytes % 4 == 0)
-    scatter_kernel<uint32_t><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots,
-                                                    local_rank, tile_offsets, bb, occupied);
+    MOE_SCATTER(uint32_t);
   else
-    scatter_kernel<uint16_t><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots,
-                                                    local_rank, tile_offsets, bb, occupied);
+    MOE_SCATTER(uint16_t);
+#undef MOE_SCATTER
   return (int)cudaGetLastError();
 }
 

@@ -1,0 +1,303 @@
+"""Expert parallelism for the MoE layer across the GPUs of one NVSwitch box.
+
+Partitioning: rank r holds a contiguous block of tokens and
+the contiguous expert block [r*E/p, (r+1)*E/p) (planner.py:101-109, with
+E % p == 0 as planner.py:202-206 requires). The gate (and the Residual-MoE
+shared MLP) is replicated.
+
+Capacity is GLOBAL: cap = ceil(cf * S_total * k / E), and slots are counted
+over the whole batch in token-major order. Because token-major order over the
+concatenated batch equals rank-major order over contiguous shards, a token's
+global slot = (assignments to its expert on lower ranks) + (its slot within
+its own shard). One all-gather of the per-rank (E,) expert counts gives every
+rank those prefixes, so routing, slots and the dropped set are bit-identical
+to ``build_dispatch_plan`` run on the whole batch at any p.
+
+Exchange (one NCCL all-to-all each way over NVLink):
+  send buffer on rank r : kept rows ordered (owner rank, expert, slot)
+  receive buffer        : [source rank][local expert][rows in slot order]
+                          (commsim's delivery contract: ordered by source,
+                          commsim.py:188-189, flat schedule :239-277)
+  the grouped GEMM runs directly on the receive layout (one group per
+  (source, local expert) segment), the results go back with the inverse
+  all-to-all, and the combine gathers them by the row index dispatch wrote.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .arch import FFN_MULT, DenseFfn, LayerSpec, MoeLayerParams, _grouped_gemm, _Phases, _t
+from .gating import GatingConfig
+from .tensor import ShapeError
+
+__all__ = ["ExchangePlan", "make_exchange_plan", "gather_counts", "exchange_rows", "EPMoeLayer"]
+
+
+@dataclass
+class ExchangePlan:
+    world: int
+    rank: int
+    E: int
+    E_loc: int
+    cap: int
+    counts: np.ndarray          # (world, E) assignments per rank and expert (before drops)
+    base: np.ndarray            # (world, E) global slot of each rank's first assignment to e
+    kept: np.ndarray            # (world, E) kept assignments per rank and expert
+    send_row_base: np.ndarray   # (E,) this rank's send-buffer start row per expert
+    send_splits: list           # rows to each destination rank
+    recv_splits: list           # rows from each source rank
+    seg_row_start: np.ndarray   # (world*E_loc,) receive-buffer start of (src, local expert)
+    seg_rows: np.ndarray        # (world*E_loc,)
+    seg_weight: np.ndarray      # (world*E_loc,) local expert index
+    expert_load: np.ndarray     # (E_loc,) kept rows per local expert (= min(total, cap))
+
+    @property
+    def n_send(self) -> int:
+        return int(sum(self.send_splits))
+
+    @property
+    def n_recv(self) -> int:
+        return int(sum(self.recv_splits))
+
+
+def make_exchange_plan(counts: np.ndarray, cap: int, rank: int, num_experts: int) -> ExchangePlan:
+    """Host-side split arithmetic from the all-gathered (world, E) counts."""
+    counts = np.asarray(counts, dtype=np.int64)
+    world, E = counts.shape
+    if E != num_experts or E % world:
+        raise ValueError(f"E={E} must equal num_experts and divide evenly over {world} ranks")
+    e_loc = E // world
+    base = np.zeros_like(counts)
+    base[1:] = np.cumsum(counts, axis=0)[:-1]
+    kept = np.clip(cap - base, 0, counts)
+    mine = kept[rank]
+    send_row_base = np.zeros(E, dtype=np.int64)
+    send_row_base[1:] = np.cumsum(mine)[:-1]
+    send_splits = [int(mine[o * e_loc:(o + 1) * e_loc].sum()) for o in range(world)]
+    lo, hi = rank * e_loc, (rank + 1) * e_loc
+    recv_splits = [int(kept[s, lo:hi].sum()) for s in range(world)]
+    seg_rows = kept[:, lo:hi].reshape(-1)
+    seg_row_start = np.zeros_like(seg_rows)
+    seg_row_start[1:] = np.cumsum(seg_rows)[:-1]
+    seg_weight = np.tile(np.arange(e_loc), world)
+    expert_load = np.minimum(counts[:, lo:hi].sum(axis=0), cap)
+    assert int(expert_load.sum()) == int(seg_rows.sum())
+    return ExchangePlan(world=world, rank=rank, E=E, E_loc=e_loc, cap=cap, counts=counts,
+                        base=base, kept=kept, send_row_base=send_row_base,
+                        send_splits=send_splits, recv_splits=recv_splits,
+                        seg_row_start=seg_row_start, seg_rows=seg_rows, seg_weight=seg_weight,
+                        expert_load=expert_load)
+
+
+def gather_counts(out_flat: torch.Tensor, totals: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather every rank's (E,) expert counts into a flat (world*E,) tensor."""
+    dist.all_gather_into_tensor(out_flat, totals, group=group)
+    return out_flat.view(-1, totals.numel())
+
+
+def exchange_rows(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group=None):
+    """One flat all-to-all of variable row counts (NCCL on GPU, gloo on CPU)."""
+    n_out, n_in = int(sum(out_splits)), int(sum(in_splits))
+    dist.all_to_all_single(out[:n_out], inp[:n_in], output_split_sizes=list(out_splits),
+                           input_split_sizes=list(in_splits), group=group)
+    return out[:n_out]
+
+
+class EPMoeLayer:
+    """One MoE layer sharded over the ranks of ``group`` (bf16, tcgen05 path)."""
+
+    def __init__(self, spec: LayerSpec, gate_w, local_experts, shared=None, group=None,
+                 dtype=torch.bfloat16, device=None) -> None:
+        if spec.kind != "moe":
+            raise ShapeError("EPMoeLayer needs a moe LayerSpec")
+        if dtype != torch.bfloat16:
+            raise TypeError("the expert-parallel path is bf16 (tcgen05)")
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        E, M = spec.experts, spec.hidden
+        if E % self.world:
+            raise ValueError(f"{E} experts do not divide over {self.world} ranks (planner.py:202-206)")
+        dev = _lib.require_device(None) if device is None else torch.device(device)
+        self.spec, self.dev, self.dtype = spec, dev, dtype
+        self.E, self.M, self.F, self.k = E, M, FFN_MULT * M, spec.gating.k
+        self.E_loc = E // self.world
+        if len(local_experts) != self.E_loc:
+            raise ShapeError(f"{len(local_experts)} local experts, expected {self.E_loc}")
+        gw = _t(gate_w, dev, torch.float32)
+        self.epad = max(32, 1 << (E - 1).bit_length())
+        self.wg = torch.zeros((self.epad, M), dtype=torch.bfloat16, device=dev)
+        self.wg[:E] = gw.t().to(torch.bfloat16)
+        F = self.F
+        self.w1 = torch.empty((self.E_loc * F, M), dtype=torch.bfloat16, device=dev)
+        self.w2 = torch.empty((self.E_loc * M, F), dtype=torch.bfloat16, device=dev)
+        self.b1 = torch.empty((self.E_loc, F), dtype=torch.float32, device=dev)
+        self.b2 = torch.empty((self.E_loc, M), dtype=torch.float32, device=dev)
+        for i, p in enumerate(local_experts):  # one expert at a time: bounded peak memory
+            self.w1[i * F:(i + 1) * F] = _t(p.w1, dev, torch.bfloat16).t()
+            self.w2[i * M:(i + 1) * M] = _t(p.w2, dev, torch.bfloat16).t()
+            self.b1[i] = _t(p.b1, dev, torch.float32).reshape(F)
+            self.b2[i] = _t(p.b2, dev, torch.float32).reshape(M)
+        self.shared = DenseFfn(shared, M, dtype, dev) if spec.residual else None
+        self._ws: dict = {}
+        self.last_plan: ExchangePlan | None = None
+
+    @classmethod
+    def from_params(cls, spec: LayerSpec, params: MoeLayerParams, group=None, **kw):
+        """Take this rank's expert block out of full (replicated) parameters."""
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        e_loc = spec.experts // world
+        local = params.experts[rank * e_loc:(rank + 1) * e_loc]
+        return cls(spec, params.gate_w, local, params.shared, group=group, **kw)
+
+    @classmethod
+    def synthetic(cls, S: int, M: int, E: int, k: int, cf: float, dev, seed: int = 0, group=None):
+        """Random-init layer of the named shape (N(0,1)*0.1 weights, zero biases,
+        arch.py:347-365), generated on device per expert so every rank draws
+        the same gate and its own expert block."""
+        from .arch import FfnParams
+
+        spec = LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, k, cf))
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        e_loc = E // world
+        g = torch.Generator(device=dev).manual_seed(seed)
+        gate_w = torch.randn(M, E, device=dev, generator=g) * 0.1
+        F = FFN_MULT * M
+        experts = []
+        zb1, zb2 = torch.zeros(1, F, device=dev), torch.zeros(1, M, device=dev)
+        for e in range(rank * e_loc, (rank + 1) * e_loc):
+            ge = torch.Generator(device=dev).manual_seed(seed * 100003 + e + 1)
+            w1 = torch.randn(M, F, device=dev, generator=ge, dtype=torch.bfloat16) * 0.1
+            w2 = torch.randn(F, M, device=dev, generator=ge, dtype=torch.bfloat16) * 0.1
+            experts.append(FfnParams(w1, zb1, w2, zb2))
+        return cls(spec, gate_w, experts, None, group=group, device=dev)
+
+    # ------------------------------------------------------------------
+    def _workspace(self, S: int) -> dict:
+        ws = self._ws.get(S)
+        if ws is not None:
+            return ws
+        self._ws.clear()
+        dev, E, M, F, k = self.dev, self.E, self.M, self.F, self.k
+        T = (S + _lib.ROUTE_TILE - 1) // _lib.ROUTE_TILE
+        i32 = dict(dtype=torch.int32, device=dev)
+        ws = dict(
+            T=T, ids=torch.empty((S, k), **i32), slots=torch.empty((S, k), **i32),
+            row_index=torch.empty((S, k), **i32), local_rank=torch.empty((S, k), **i32),
+            gp=torch.empty((S, k), dtype=torch.float32, device=dev),
+            tile_counts=torch.empty((max(T, 1), E), **i32),
+            tile_offsets=torch.empty((max(T, 1), E), **i32),
+            totals=torch.empty(E, **i32), kept=torch.empty(E, **i32),
+            counts=torch.empty(self.world * E, **i32),
+            send=torch.empty((max(S * k, 1), M), dtype=self.dtype, device=dev),
+            ret=torch.empty((max(S * k, 1), M), dtype=self.dtype, device=dev),
+        )
+        if self.shared is not None:
+            ws["hs"] = torch.empty((S, F), dtype=self.dtype, device=dev)
+            ws["ys"] = torch.empty((S, M), dtype=self.dtype, device=dev)
+        self._ws[S] = ws
+        return ws
+
+    def _recv_buffers(self, ws: dict, rows: int) -> None:
+        if ws.get("recv_rows", -1) >= rows:
+            return
+        rows = max(rows, 1)
+        ws["recv"] = torch.empty((rows, self.M), dtype=self.dtype, device=self.dev)
+        ws["h"] = torch.empty((rows, self.F), dtype=self.dtype, device=self.dev)
+        ws["y"] = torch.empty((rows, self.M), dtype=self.dtype, device=self.dev)
+        ws["recv_rows"] = rows
+
+    def __call__(self, x, out=None, timer=None):
+        return self.forward(x, out, timer)
+
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, timer=None):
+        """out = x + combine(experts(dispatch(x))) [+ shared(x)] for this rank's
+        tokens, experts evaluated on their owner ranks."""
+        if x.device != self.dev:
+            x = x.to(self.dev, non_blocking=True)
+        x = x.to(self.dtype).contiguous()
+        if x.dim() != 2 or x.shape[1] != self.M:
+            raise ShapeError(f"batch width {tuple(x.shape)} does not match layer hidden {self.M}")
+        S = x.shape[0]
+        out = torch.empty_like(x) if out is None else out
+        ws = self._workspace(S)
+        E, M, F, k = self.E, self.M, self.F, self.k
+        st = _lib.stream_ptr()
+        ph = _Phases(timer)
+        ids, gp, lr, tc = ws["ids"], ws["gp"], ws["local_rank"], ws["tile_counts"]
+        ph("gate")
+        if S:
+            _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k, None,
+                      ids.data_ptr(), gp.data_ptr(), lr.data_ptr(), tc.data_ptr(), st)
+        # local per-expert counts (cap irrelevant here)
+        _lib.call("moe_plan_scan", tc.data_ptr(), S, E, 2 ** 62, None,
+                  ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
+                  st)
+        ph("counts_allgather")
+        counts = gather_counts(ws["counts"], ws["totals"], self.group)
+        counts = counts.cpu().numpy()  # the one host sync: splits for NCCL
+        s_total = int(counts.sum()) // k
+        cap = self.spec.gating.capacity(s_total)
+        plan = make_exchange_plan(counts, cap, self.rank, E)
+        self.last_plan = plan
+        ph("scan")
+        tables = np.concatenate([plan.base[self.rank], plan.send_row_base, plan.seg_row_start,
+                                 plan.seg_rows, plan.seg_weight]).astype(np.int32)
+        tab = torch.from_numpy(tables).to(self.dev, non_blocking=True)
+        base_d, row_base_d = tab[:E], tab[E:2 * E]
+        G = self.world * self.E_loc
+        seg_start_d, seg_rows_d, seg_w_d = tab[2 * E:2 * E + G], tab[2 * E + G:2 * E + 2 * G], \
+            tab[2 * E + 2 * G:2 * E + 3 * G]
+        _lib.call("moe_plan_scan", tc.data_ptr(), S, E, cap, base_d.data_ptr(),
+                  ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
+                  st)
+        ph("dispatch")
+        if S:
+            _lib.call("moe_dispatch_ep", x.data_ptr(), S, M * 2, E, k, cap, ids.data_ptr(),
+                      lr.data_ptr(), ws["tile_offsets"].data_ptr(), base_d.data_ptr(),
+                      row_base_d.data_ptr(), ws["slots"].data_ptr(), ws["row_index"].data_ptr(),
+                      ws["send"].data_ptr(), st)
+        ph("all_to_all_dispatch")
+        self._recv_buffers(ws, plan.n_recv)
+        recv = exchange_rows(ws["recv"], ws["send"], plan.recv_splits, plan.send_splits,
+                             self.group)
+        n_recv = plan.n_recv
+        max_rows = int(plan.seg_rows.max()) if plan.seg_rows.size else 0
+        if n_recv and max_rows:
+            ph("gemm1")
+            _lib.call("moe_grouped_gemm_bf16", recv.data_ptr(), n_recv, M, self.w1.data_ptr(),
+                      self.E_loc * F, F, self.b1.data_ptr(), ws["h"].data_ptr(), G,
+                      seg_start_d.data_ptr(), 0, seg_rows_d.data_ptr(), 0, seg_w_d.data_ptr(),
+                      max_rows, _lib.MOE_ACT_GELU, st)
+            ph("gemm2")
+            _lib.call("moe_grouped_gemm_bf16", ws["h"].data_ptr(), n_recv, F, self.w2.data_ptr(),
+                      self.E_loc * M, M, self.b2.data_ptr(), ws["y"].data_ptr(), G,
+                      seg_start_d.data_ptr(), 0, seg_rows_d.data_ptr(), 0, seg_w_d.data_ptr(),
+                      max_rows, _lib.MOE_ACT_NONE, st)
+        ph("all_to_all_return")
+        exchange_rows(ws["ret"], ws["y"], plan.send_splits, plan.recv_splits, self.group)
+        shared_out = None
+        if self.shared is not None:
+            ph("shared_mlp")
+            shared_out = self.shared(x, ws["hs"], ws["ys"])
+        ph("combine")
+        if S:
+            _lib.call("moe_combine", ws["ret"].data_ptr(), _lib.MOE_BF16, S, M, E, k, cap,
+                      ids.data_ptr(), ws["slots"].data_ptr(), ws["row_index"].data_ptr(),
+                      gp.data_ptr(), _lib.MOE_F32, x.data_ptr(), _lib.ptr(shared_out),
+                      out.data_ptr(), 1, st)
+        ph(None)
+        return out
+
+    def kept_assignments(self, S: int) -> int:
+        return int(self.last_plan.kept[self.rank].sum()) if self.last_plan is not None else 0
+
+    def plan(self, S: int):
+        ws = self._ws[S]
+        return ws["ids"], ws["gp"], ws["slots"], self.last_plan
