@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
-python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err; cat gpurun_out/bench.json
+timeout 600 python -m pytest tests/test_gpu_gemm.py -x -q -p no:cacheprovider 2>&1 | tail -3
+MOE_GEMM_VARIANT=1 timeout 600 python -m pytest tests/test_gpu_gemm.py -x -q -p no:cacheprovider 2>&1 | tail -2
+python tools/gemm_bench.py --rounds 3

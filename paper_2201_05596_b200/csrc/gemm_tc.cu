@@ -21,6 +21,7 @@
 
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 namespace moe {
@@ -29,7 +30,14 @@ enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2 };
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
-constexpr int kThreads = 192;
+// warps 0-1: TMA producer, MMA issuer; then the epilogue warps. The expert
+// GEMMs use 8 epilogue warps (2 per TMEM lane quarter, each owning half of the
+// tile's columns) so two warps per scheduler hide the epilogue's latencies;
+// the gate epilogue (thread = token, full row of logits) uses 4.
+template <int EW>
+constexpr int threads_for() {
+  return 64 + 32 * EW;
+}
 constexpr int kMaxGroups = 2048;
 
 struct GemmArgs {
@@ -52,10 +60,14 @@ struct GemmArgs {
   int32_t* tile_counts;       // [T, E]
 };
 
-template <int BN, int STAGES>
+// CG = 1: one CTA computes a BM x BN tile (tcgen05.mma.cta_group::1, M=128).
+// CG = 2: a 2-CTA cluster computes a (2*BM) x BN tile with cta_group::2 (M=256):
+// each CTA loads its own 128 rows of A and BN/2 rows of B, the leader CTA issues
+// the MMAs for the pair, each CTA's TMEM holds its 128 accumulator rows.
+template <int BN, int STAGES, int CG>
 struct Smem {
   static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOff = STAGES * kStageBytes;
   static constexpr int kBarBytes = (2 * STAGES + 4) * 8 + 16;
@@ -68,11 +80,12 @@ constexpr uint32_t tmem_cols() {
   return (2 * BN) < 32 ? 32 : (2 * BN);
 }
 
-template <int BN, int STAGES, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int STAGES, int EPI, int CG, int EW>
+__global__ void __launch_bounds__(threads_for<EW>(), 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
-  using L = Smem<BN, STAGES>;
+  using L = Smem<BN, STAGES, CG>;
+  constexpr int TM = BM * CG;  // rows per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -87,15 +100,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = lane_id();
   const int G = args.G;
   const int n_blocks = (args.N + BN - 1) / BN;
+  const uint32_t cta = CG == 2 ? cluster_ctarank() : 0;  // rank inside the CTA pair
+  const bool leader = cta == 0;
+  const int work_id = blockIdx.x / CG, work_stride = gridDim.x / CG;
+  if constexpr (CG == 2) cluster_sync();  // both CTAs resident before the paired TMEM alloc
 
-  // ---- per-CTA tile table: tile_start[g] = sum_{g'<g} ceil(rows/BM) * n_blocks
+  // ---- per-CTA tile table: tile_start[g] = sum_{g'<g} ceil(rows/TM) * n_blocks
   if (warp == 0) {
     const int per = (G + 31) / 32;
     const int g0 = lane * per;
     int local = 0;
     for (int g = g0; g < min(G, g0 + per); ++g) {
       const int64_t r = args.rows ? args.rows[g] : args.rows_const;
-      local += (int)((r + BM - 1) / BM) * n_blocks;
+      local += (int)((r + TM - 1) / TM) * n_blocks;
     }
     int incl = local;
 #pragma unroll
@@ -107,31 +124,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int g = g0; g < min(G, g0 + per); ++g) {
       tile_start[g] = run;
       const int64_t r = args.rows ? args.rows[g] : args.rows_const;
-      run += (int)((r + BM - 1) / BM) * n_blocks;
+      run += (int)((r + TM - 1) / TM) * n_blocks;
     }
     if (lane == 31) tile_start[G] = incl;
   }
   if (warp == 1) {
     if (lane == 0) {
       for (int s = 0; s < STAGES; ++s) {
-        mbar_init(&full[s], 1);
+        mbar_init(&full[s], CG);  // CG=2: the peer's producer arrives remotely on the leader's
         mbar_init(&empty[s], 1);
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], 4);
+        mbar_init(&tempty[a], EW * CG);  // every epilogue warp of the pair arrives
       }
       mbar_fence_init();
     }
     __syncwarp();
-    tmem_alloc(tmem_slot, tmem_cols<BN>());
+    if constexpr (CG == 2)
+      tmem_alloc_cg2(tmem_slot, tmem_cols<BN>());
+    else
+      tmem_alloc(tmem_slot, tmem_cols<BN>());
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();  // barrier inits visible to the peer before any remote arrive
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = tile_start[G];
@@ -142,32 +165,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     while (tile_start[g + 1] <= tile) ++g;
     const int local = tile - tile_start[g];
     const int64_t r = args.rows ? args.rows[g] : args.rows_const;
-    const int mblocks = (int)((r + BM - 1) / BM);
+    const int mblocks = (int)((r + TM - 1) / TM);
     nb = local / mblocks;
     mb = local - nb * mblocks;
   };
 
   if (warp == 0) {
-    // ===================== TMA producer
+    // ===================== TMA producer (both CTAs of a pair load their halves)
     int stage = 0;
     uint32_t phase = 0;
     int g = 0;
     const int num_kb = (args.K + BK - 1) / BK;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int tile = work_id; tile < total_tiles; tile += work_stride) {
       int mb, nb;
       decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
-      const int a_row = (int)(rs + (int64_t)mb * BM);
-      const int b_row = w * args.N + nb * BN;
+      const int a_row = (int)(rs + (int64_t)mb * TM + cta * BM);
+      const int b_row = w * args.N + nb * BN + cta * (BN / CG);
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
-          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-          tma_load_2d(sa, &map_a, &full[stage], kb * BK, a_row);
-          tma_load_2d(sb, &map_b, &full[stage], kb * BK, b_row);
+          if constexpr (CG == 2) {
+            tma_load_2d_cg2(sa, &map_a, &full[stage], kb * BK, a_row);
+            tma_load_2d_cg2(sb, &map_b, &full[stage], kb * BK, b_row);
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+            else
+              mbar_arrive_cluster(&full[stage], 0);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+            tma_load_2d(sa, &map_a, &full[stage], kb * BK, a_row);
+            tma_load_2d(sb, &map_b, &full[stage], kb * BK, b_row);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -177,14 +209,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (lane 0 issues, whole warp waits)
-    constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
+    // ===================== MMA issuer (leader CTA only; lane 0 issues, whole warp waits)
+    constexpr uint32_t idesc = make_idesc_bf16(TM, BN);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     const int num_kb = (args.K + BK - 1) / BK;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int tile = work_id; leader && tile < total_tiles; tile += work_stride) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -199,9 +231,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             // advance 16 bf16 = 32 B along K inside the swizzle row (>>4 -> +2)
-            umma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+            if constexpr (CG == 2)
+              umma_bf16_cg2(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+            else
+              umma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (CG == 2)
+            umma_commit_cg2(&empty[stage], 0x3);  // frees the stage in both CTAs
+          else
+            umma_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -209,7 +247,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
-      if (lane == 0) umma_commit(&tfull[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          umma_commit_cg2(&tfull[acc], 0x3);
+        else
+          umma_commit(&tfull[acc]);
+      }
       __syncwarp();
       if (++acc == 2) {
         acc = 0;
@@ -219,24 +262,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ===================== epilogue warps 2..5
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int row_in_tile = quarter * 32 + lane;
+    constexpr int kColSplit = EW / 4;    // warps sharing a quarter split the columns
+    const int col_part = (int)(warp - 2) / 4;          // 0 .. kColSplit-1
+    constexpr int kChunks = BN / 32 / kColSplit;       // 32-column chunks per warp
+    const int row_in_tile = cta * BM + quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
     int g = 0;
     const int N = args.N;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int tile = work_id; tile < total_tiles; tile += work_stride) {
       int mb, nb;
       decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int64_t rows_g = args.rows ? args.rows[g] : args.rows_const;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
-      const int64_t local_row = (int64_t)mb * BM + row_in_tile;
+      const int64_t local_row = (int64_t)mb * TM + row_in_tile;
       const bool valid = local_row < rows_g;
       const int64_t out_row = rs + local_row;
 
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_addr = tmem_base + ((quarter * 32) << 16) + acc * BN;
+      const uint32_t t_addr = tmem_base + ((quarter * 32) << 16) + acc * BN +
+                              (EPI != EPI_GATE ? col_part * kChunks * 32 : 0);
 
       if constexpr (EPI != EPI_GATE) {
         const float* bias = args.bias ? args.bias + (int64_t)w * N : nullptr;
@@ -247,8 +294,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[2][32];
         tmem_ld_32x32b_x32(t_addr, r[0]);
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          const int col0 = nb * BN + c * 32;
+        for (int c = 0; c < kChunks; ++c) {
+          const int col0 = nb * BN + (col_part * kChunks + c) * 32;
           float bv[32];
           if (bias != nullptr && vec_ok && col0 + 32 <= N) {
             const float4* b4 = reinterpret_cast<const float4*>(bias + col0);
@@ -263,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               bv[i] = (bias != nullptr && col0 + i < N) ? __ldg(bias + col0 + i) : 0.f;
           }
           tmem_ld_wait_regs(r[c & 1]);
-          if (c + 1 < BN / 32) tmem_ld_32x32b_x32(t_addr + (c + 1) * 32, r[(c + 1) & 1]);
+          if (c + 1 < kChunks) tmem_ld_32x32b_x32(t_addr + (c + 1) * 32, r[(c + 1) & 1]);
           if (!valid || col0 >= N) continue;
           float v[32];
 #pragma unroll
@@ -291,7 +338,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if constexpr (CG == 2)
+            mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA reuses this accumulator
+          else
+            mbar_arrive(&tempty[acc]);
+        }
       } else {
         // ---------------- gate epilogue: thread = token row, BN >= E columns
         const int E = args.E;
@@ -394,10 +446,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();  // the peer's TMEM is written by the leader's MMAs: free only when both done
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, tmem_cols<BN>());
+    if constexpr (CG == 2)
+      tmem_dealloc_cg2(tmem_base, tmem_cols<BN>());
+    else
+      tmem_dealloc(tmem_base, tmem_cols<BN>());
   }
 }
 
@@ -440,21 +498,34 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EPI>
+template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
                      int64_t max_tiles, cudaStream_t st) {
-  using L = Smem<BN, STAGES>;
-  auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI>;
+  using L = Smem<BN, STAGES, CG>;
+  auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return (int)e;
     attr_done = true;
   }
-  int grid = num_sms();
-  if (max_tiles < grid) grid = (int)(max_tiles < 1 ? 1 : max_tiles);
-  kern<<<grid, kThreads, L::kTotal, st>>>(ma, mb, args);
-  return (int)cudaGetLastError();
+  int64_t grid = num_sms();
+  if (max_tiles * CG < grid) grid = max_tiles < 1 ? CG : max_tiles * CG;
+  grid -= grid % CG;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(threads_for<EW>());
+  cfg.dynamicSmemBytes = L::kTotal;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, args);
+  return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
 int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
@@ -467,10 +538,19 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   if (N <= 32) BN = 32;
   else if (N <= 64) BN = 64;
   else if (N <= 128) BN = 128;
+  // 2-CTA 256x256 tiles for the big expert GEMMs; 1-CTA 128-row tiles when groups are
+  // small (decode) or N is narrow
+  // MOE_GEMM_VARIANT (tuning knob, default 0): 0 = 2-CTA + 8 epilogue warps,
+  // 1 = 2-CTA + 4 epilogue warps, 2 = 1-CTA + 4 epilogue warps
+  static const int variant = [] {
+    const char* v = getenv("MOE_GEMM_VARIANT");
+    return v ? atoi(v) : 0;
+  }();
+  const int CG = (BN == 256 && max_group_rows > BM && variant != 2) ? 2 : 1;
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, a_rows, K, BM);
   if (rc) return rc;
-  rc = make_map(&mb, B, b_rows, K, BN);
+  rc = make_map(&mb, B, b_rows, K, BN / CG);
   if (rc) return rc;
   GemmArgs a{};
   a.bias = bias;
@@ -484,17 +564,26 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.rows_const = rows_const;
   a.weight_idx = weight_idx;
   const int64_t nblk = (N + BN - 1) / BN;
-  const int64_t max_tiles = (int64_t)G * ((max_group_rows + BM - 1) / BM) * nblk;
+  const int64_t tm = (int64_t)BM * CG;
+  const int64_t max_tiles = (int64_t)G * ((max_group_rows + tm - 1) / tm) * nblk;
   if (max_tiles == 0) return 0;
   const bool gelu = act == 1;
+  if (CG == 2 && variant == 1)
+    return gelu ? launch_tc<256, 6, EPI_BIAS_GELU, 2, 4>(ma, mb, a, max_tiles, st)
+                : launch_tc<256, 6, EPI_BIAS, 2, 4>(ma, mb, a, max_tiles, st);
+  if (CG == 2)
+    return gelu ? launch_tc<256, 6, EPI_BIAS_GELU, 2, 8>(ma, mb, a, max_tiles, st)
+                : launch_tc<256, 6, EPI_BIAS, 2, 8>(ma, mb, a, max_tiles, st);
 #define MOE_TC(BN_, ST_)                                                            \
-  return gelu ? launch_tc<BN_, ST_, EPI_BIAS_GELU>(ma, mb, a, max_tiles, st)        \
-              : launch_tc<BN_, ST_, EPI_BIAS>(ma, mb, a, max_tiles, st)
+  return gelu ? launch_tc<BN_, ST_, EPI_BIAS_GELU, 1, (BN_ >= 64 ? 8 : 4)>(ma, mb, a, max_tiles, st) \
+              : launch_tc<BN_, ST_, EPI_BIAS, 1, (BN_ >= 64 ? 8 : 4)>(ma, mb, a, max_tiles, st)
   switch (BN) {
     case 32: MOE_TC(32, 8);
     case 64: MOE_TC(64, 8);
     case 128: MOE_TC(128, 6);
-    default: MOE_TC(256, 4);
+    default:
+      return gelu ? launch_tc<256, 4, EPI_BIAS_GELU, 1, 4>(ma, mb, a, max_tiles, st)
+                  : launch_tc<256, 4, EPI_BIAS, 1, 4>(ma, mb, a, max_tiles, st);
   }
 #undef MOE_TC
 }
