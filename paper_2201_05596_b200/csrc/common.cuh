@@ -225,6 +225,16 @@ MOE_DEV void tma_load_2d_cg2(void* smem_dst, const CUtensorMap* map, uint64_t* b
       : "memory");
 }
 
+MOE_DEV void tma_load_2d_cg2_hint(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                  int32_t c1, uint64_t policy) {
+  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+
 MOE_DEV void tmem_alloc_cg2(uint32_t* smem_dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    smem_u32(smem_dst)),
