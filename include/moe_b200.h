@@ -95,6 +95,14 @@ int moe_dispatch(const void* x, int64_t S, int64_t row_bytes, int E, int k, int6
                  const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
                  int32_t* slots, void* buf, void* stream);
 
+/* moe_dispatch plus, for the fused-combine path (k=1): row_token / row_prob
+ * (E*cap, the token and gate probability behind each expert-buffer row) and,
+ * when out_dropped is given, out_dropped[t] = x[t] for fully dropped tokens. */
+int moe_dispatch_fused(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                       const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                       const float* gate_probs, int32_t* slots, void* buf, int32_t* row_token,
+                       float* row_prob, void* out_dropped, void* stream);
+
 /* Expert-parallel dispatch into the all-to-all send buffer. tile_offsets come
  * from moe_plan_scan with rank_base = slot_base (global slots); a kept
  * assignment (slot < cap) goes to send row row_base[e] + slot - slot_base[e]
@@ -137,6 +145,19 @@ int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, i
                           const int32_t* row_start, int64_t row_stride, const int32_t* rows,
                           int64_t rows_const, const int32_t* weight_idx, int64_t max_group_rows,
                           int act, void* stream);
+
+/* GEMM2 of a k=1 layer with combine_tokens and the residual add fused into the
+ * epilogue (gating.py:281-307, arch.py:389): for every expert-buffer row r
+ *   out[row_token[r]] = x_resid[row_token[r]] + row_prob[r] * (A[r] @ B_w^T + bias_w)
+ * row_token / row_prob come from moe_dispatch_fused, which also writes
+ * out[t] = x[t] for fully dropped tokens. Other arguments as above. */
+int moe_grouped_gemm_bf16_combine(const void* A, int64_t a_rows, int K, const void* B,
+                                  int64_t b_rows, int N, const float* bias, int num_groups,
+                                  const int32_t* row_start, int64_t row_stride,
+                                  const int32_t* rows, int64_t rows_const,
+                                  const int32_t* weight_idx, int64_t max_group_rows,
+                                  const int32_t* row_token, const float* row_prob,
+                                  const void* x_resid, void* out, void* stream);
 
 /* fp32 SIMT variant (parity path). B f32 in the reference layout: weight w is
  * (K, N) row-major at B + w*K*N. */

@@ -41,10 +41,13 @@ SIGNATURES = {
     "moe_scatter": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P]),
     "moe_dispatch": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
     "moe_dispatch_ep": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "moe_dispatch_fused": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "moe_combine": (_I, [_P, _I, _L, _I, _I, _I, _L, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P]),
     "moe_gate_gemm_bf16": (_I, [_P, _P, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "moe_grouped_gemm_bf16": (_I, [_P, _L, _I, _P, _L, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L,
                                    _I, _P]),
+    "moe_grouped_gemm_bf16_combine": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _L, _P, _L, _P,
+                                           _L, _P, _P, _P, _P, _P]),
     "moe_grouped_gemm_f32": (_I, [_P, _I, _P, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L, _I, _P]),
 }
 

@@ -213,7 +213,7 @@ class MoeLayer:
     """
 
     def __init__(self, spec: LayerSpec, params: MoeLayerParams, dtype=torch.bfloat16,
-                 device=None) -> None:
+                 device=None, fuse_combine: bool = True) -> None:
         if spec.kind != "moe":
             raise ValidationError("MoeLayer needs a moe LayerSpec")
         dev = _lib.require_device(None) if device is None else torch.device(device)
@@ -252,6 +252,9 @@ class MoeLayer:
                        if (spec.residual and params.shared is not None) else None)
         if spec.residual and params.shared is None:
             raise ValidationError("residual layer needs shared MLP params")
+        # k=1 bf16 layers without a shared MLP fold combine + residual into GEMM2
+        self.fused_combine = bool(fuse_combine and self.dtype == torch.bfloat16 and
+                                  self.k == 1 and self.shared is None)
         self._ws: dict = {}
 
     # -- workspace -----------------------------------------------------------
@@ -278,6 +281,9 @@ class MoeLayer:
         )
         if dt == torch.float32:
             ws["logits"] = torch.empty((S, E), dtype=torch.float32, device=dev)
+        if self.fused_combine:
+            ws["row_token"] = torch.empty(max(E * cap, 1), **i32)
+            ws["row_prob"] = torch.empty(max(E * cap, 1), dtype=torch.float32, device=dev)
         if self.shared is not None:
             ws["hs"] = torch.empty((S, F), dtype=dt, device=dev)
             ws["ys"] = torch.empty((S, M), dtype=dt, device=dev)
@@ -326,6 +332,22 @@ class MoeLayer:
         _lib.call("moe_plan_scan", tc.data_ptr(), S, E, cap, None, ws["tile_offsets"].data_ptr(),
                   ws["totals"].data_ptr(), ws["load"].data_ptr(), st)
         ph("dispatch")
+        if self.fused_combine:
+            _lib.call("moe_dispatch_fused", x.data_ptr(), S, M * x.element_size(), E, k, cap,
+                      ids.data_ptr(), lr.data_ptr(), ws["tile_offsets"].data_ptr(), gp.data_ptr(),
+                      ws["slots"].data_ptr(), ws["xbuf"].data_ptr(), ws["row_token"].data_ptr(),
+                      ws["row_prob"].data_ptr(), out.data_ptr(), st)
+            if cap > 0:
+                ph("gemm1")
+                _grouped_gemm(self.dtype, ws["xbuf"], E * cap, M, self.w1, F, self.b1, ws["h"], E,
+                              None, cap, ws["load"], 0, cap, _lib.MOE_ACT_GELU)
+                ph("gemm2")  # + combine + residual in the epilogue
+                _lib.call("moe_grouped_gemm_bf16_combine", ws["h"].data_ptr(), E * cap, F,
+                          self.w2.data_ptr(), E * M, M, self.b2.data_ptr(), E, None, cap,
+                          ws["load"].data_ptr(), 0, None, cap, ws["row_token"].data_ptr(),
+                          ws["row_prob"].data_ptr(), x.data_ptr(), out.data_ptr(), st)
+            ph(None)
+            return out
         _lib.call("moe_dispatch", x.data_ptr(), S, M * x.element_size(), E, k, cap, ids.data_ptr(),
                   lr.data_ptr(), ws["tile_offsets"].data_ptr(), ws["slots"].data_ptr(),
                   ws["xbuf"].data_ptr(), st)

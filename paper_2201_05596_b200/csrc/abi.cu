@@ -99,8 +99,12 @@ int moe_scatter(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64
   CHECK(row_bytes % 2 == 0);
   if (S == 0 || cap == 0) return MOE_OK;
   CHECK(x && ids && slots && buf);
-  return moe::launch_scatter(x, S, row_bytes, k, E, cap, ids, const_cast<int32_t*>(slots), nullptr,
-                             nullptr, buf, occupied, nullptr, nullptr, nullptr, S_(stream));
+  moe::ScatterArgs a;
+  a.x = static_cast<const uint8_t*>(x);
+  a.S = S, a.row_bytes = row_bytes, a.k = k, a.E = E, a.cap = cap;
+  a.ids = ids, a.slots = const_cast<int32_t*>(slots);
+  a.buf = static_cast<uint8_t*>(buf), a.occupied = occupied;
+  return moe::launch_scatter(a, S_(stream));
 }
 
 int moe_dispatch(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
@@ -110,8 +114,31 @@ int moe_dispatch(const void* x, int64_t S, int64_t row_bytes, int E, int k, int6
         cap >= 0);
   if (S == 0) return MOE_OK;
   CHECK(x && ids && local_rank && tile_offsets && slots && (buf || cap == 0));
-  return moe::launch_scatter(x, S, row_bytes, k, E, cap, ids, slots, local_rank, tile_offsets, buf,
-                             nullptr, nullptr, nullptr, nullptr, S_(stream));
+  moe::ScatterArgs a;
+  a.x = static_cast<const uint8_t*>(x);
+  a.S = S, a.row_bytes = row_bytes, a.k = k, a.E = E, a.cap = cap;
+  a.ids = ids, a.slots = slots, a.local_rank = local_rank, a.tile_offsets = tile_offsets;
+  a.buf = static_cast<uint8_t*>(buf);
+  return moe::launch_scatter(a, S_(stream));
+}
+
+int moe_dispatch_fused(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                       const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                       const float* gate_probs, int32_t* slots, void* buf, int32_t* row_token,
+                       float* row_prob, void* out_dropped, void* stream) {
+  CHECK(S >= 0 && row_bytes >= 0 && row_bytes % 2 == 0 && E >= 1 && (k == 1 || k == 2) &&
+        cap >= 0);
+  if (S == 0) return MOE_OK;
+  CHECK(x && ids && local_rank && tile_offsets && gate_probs && slots && row_token && row_prob &&
+        (buf || cap == 0));
+  moe::ScatterArgs a;
+  a.x = static_cast<const uint8_t*>(x);
+  a.S = S, a.row_bytes = row_bytes, a.k = k, a.E = E, a.cap = cap;
+  a.ids = ids, a.slots = slots, a.local_rank = local_rank, a.tile_offsets = tile_offsets;
+  a.buf = static_cast<uint8_t*>(buf);
+  a.gate_probs = gate_probs, a.row_token = row_token, a.row_prob = row_prob;
+  a.out_dropped = static_cast<uint8_t*>(out_dropped);
+  return moe::launch_scatter(a, S_(stream));
 }
 
 int moe_dispatch_ep(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
@@ -122,8 +149,13 @@ int moe_dispatch_ep(const void* x, int64_t S, int64_t row_bytes, int E, int k, i
         cap >= 0);
   if (S == 0) return MOE_OK;
   CHECK(x && ids && local_rank && tile_offsets && slot_base && row_base && slots && row_index);
-  return moe::launch_scatter(x, S, row_bytes, k, E, cap, ids, slots, local_rank, tile_offsets,
-                             send_buf, nullptr, slot_base, row_base, row_index, S_(stream));
+  moe::ScatterArgs a;
+  a.x = static_cast<const uint8_t*>(x);
+  a.S = S, a.row_bytes = row_bytes, a.k = k, a.E = E, a.cap = cap;
+  a.ids = ids, a.slots = slots, a.local_rank = local_rank, a.tile_offsets = tile_offsets;
+  a.buf = static_cast<uint8_t*>(send_buf);
+  a.slot_base = slot_base, a.row_base = row_base, a.row_index = row_index;
+  return moe::launch_scatter(a, S_(stream));
 }
 
 int moe_combine(const void* y, int dtype, int64_t S, int M, int E, int k, int64_t cap,
@@ -161,6 +193,23 @@ int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, i
   return moe::launch_grouped_gemm_bf16(A, a_rows, K, B, b_rows, N, bias, D, num_groups, row_start,
                                        row_stride, rows, rows_const, weight_idx, max_group_rows,
                                        act, S_(stream));
+}
+
+int moe_grouped_gemm_bf16_combine(const void* A, int64_t a_rows, int K, const void* B,
+                                  int64_t b_rows, int N, const float* bias, int num_groups,
+                                  const int32_t* row_start, int64_t row_stride,
+                                  const int32_t* rows, int64_t rows_const,
+                                  const int32_t* weight_idx, int64_t max_group_rows,
+                                  const int32_t* row_token, const float* row_prob,
+                                  const void* x_resid, void* out, void* stream) {
+  CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1);
+  CHECK(max_group_rows >= 0 && rows_const >= 0);
+  if (a_rows == 0 || max_group_rows == 0) return MOE_OK;
+  CHECK(A && B && row_token && row_prob && x_resid && out);
+  return moe::launch_grouped_gemm_bf16(A, a_rows, K, B, b_rows, N, bias, nullptr, num_groups,
+                                       row_start, row_stride, rows, rows_const, weight_idx,
+                                       max_group_rows, 2, S_(stream), row_token, row_prob,
+                                       x_resid, out);
 }
 
 int moe_grouped_gemm_f32(const float* A, int K, const float* B, int N, const float* bias, float* D,

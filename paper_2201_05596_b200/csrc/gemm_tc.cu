@@ -26,7 +26,9 @@
 
 namespace moe {
 
-enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2 };
+// EPI_BIAS_COMBINE (GEMM2 of a k=1 layer): out[token(row)] = x[token] + p(row) * (acc + b2),
+// i.e. combine_tokens + the residual add of arch.py:389 fused into the epilogue.
+enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2, EPI_BIAS_COMBINE = 3 };
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
@@ -58,6 +60,11 @@ struct GemmArgs {
   float* gate_probs;          // [S, k]
   int32_t* local_rank;        // [S, k]
   int32_t* tile_counts;       // [T, E]
+  // fused combine epilogue
+  const int32_t* row_token;   // [a_rows] token of each expert-buffer row
+  const float* row_prob;      // [a_rows] its gate probability
+  const __nv_bfloat16* x_resid;  // [S, N]
+  __nv_bfloat16* out;            // [S, N]
 };
 
 // CG = 1: one CTA computes a BM x BN tile (tcgen05.mma.cta_group::1, M=128).
@@ -291,6 +298,14 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
         const float* bias = args.bias ? args.bias + (int64_t)w * N : nullptr;
         const bool vec_ok = (N % 8) == 0;
         __nv_bfloat16* drow = args.D + out_row * N;
+        const __nv_bfloat16* xrow = nullptr;
+        float prob = 0.f;
+        if constexpr (EPI == EPI_BIAS_COMBINE) {
+          const int64_t tok = valid ? args.row_token[out_row] : 0;
+          prob = valid ? args.row_prob[out_row] : 0.f;
+          drow = args.out + tok * N;
+          xrow = args.x_resid + tok * N;
+        }
         // TMEM loads double-buffered across 32-column chunks: the load of
         // chunk c+1 is in flight while chunk c is biased, activated and stored.
         uint32_t r[2][32];
@@ -311,6 +326,14 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
             for (int i = 0; i < 32; ++i)
               bv[i] = (bias != nullptr && col0 + i < N) ? __ldg(bias + col0 + i) : 0.f;
           }
+          uint4 xq[4];
+          if constexpr (EPI == EPI_BIAS_COMBINE) {
+            if (valid && vec_ok && col0 + 32 <= N) {
+              const uint4* xs = reinterpret_cast<const uint4*>(xrow + col0);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) xq[q] = __ldg(xs + q);
+            }
+          }
           tmem_ld_wait_regs(r[c & 1]);
           if (c + 1 < kChunks) tmem_ld_32x32b_x32(t_addr + (c + 1) * 32, r[(c + 1) & 1]);
           if (!valid || col0 >= N) continue;
@@ -319,6 +342,17 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
           for (int i = 0; i < 32; ++i) {
             v[i] = __uint_as_float(r[c & 1][i]) + bv[i];
             if constexpr (EPI == EPI_BIAS_GELU) v[i] = gelu_tanh_fast(v[i]);
+          }
+          if constexpr (EPI == EPI_BIAS_COMBINE) {
+            if (vec_ok && col0 + 32 <= N) {
+              const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(xq);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = fmaf(prob, v[i], __bfloat162float(xb[i]));
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (col0 + i < N) v[i] = fmaf(prob, v[i], __bfloat162float(xrow[col0 + i]));
+            }
           }
           if (vec_ok && col0 + 32 <= N) {
             uint4* dst = reinterpret_cast<uint4*>(drow + col0);
@@ -534,7 +568,8 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              int N, const float* bias, void* D, int G, const int32_t* row_start,
                              int64_t row_stride, const int32_t* rows, int64_t rows_const,
                              const int32_t* weight_idx, int64_t max_group_rows, int act,
-                             cudaStream_t st) {
+                             cudaStream_t st, const int32_t* row_token, const float* row_prob,
+                             const void* x_resid, void* out) {
   if (G < 1 || G > kMaxGroups || K < 1 || N < 1 || (K % 8) != 0) return MOE_EINVAL;
   int BN = 256;
   if (N <= 32) BN = 32;
@@ -565,11 +600,24 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.rows = rows;
   a.rows_const = rows_const;
   a.weight_idx = weight_idx;
+  a.row_token = row_token;
+  a.row_prob = row_prob;
+  a.x_resid = (const __nv_bfloat16*)x_resid;
+  a.out = (__nv_bfloat16*)out;
   const int64_t nblk = (N + BN - 1) / BN;
   const int64_t tm = (int64_t)BM * CG;
   const int64_t max_tiles = (int64_t)G * ((max_group_rows + tm - 1) / tm) * nblk;
   if (max_tiles == 0) return 0;
   const bool gelu = act == 1;
+  if (act == 2) {  // fused combine epilogue
+    if (CG == 2) return launch_tc<256, 6, EPI_BIAS_COMBINE, 2, 8>(ma, mb, a, max_tiles, st);
+    switch (BN) {
+      case 32: return launch_tc<32, 8, EPI_BIAS_COMBINE, 1, 4>(ma, mb, a, max_tiles, st);
+      case 64: return launch_tc<64, 8, EPI_BIAS_COMBINE, 1, 8>(ma, mb, a, max_tiles, st);
+      case 128: return launch_tc<128, 6, EPI_BIAS_COMBINE, 1, 8>(ma, mb, a, max_tiles, st);
+      default: return launch_tc<256, 4, EPI_BIAS_COMBINE, 1, 4>(ma, mb, a, max_tiles, st);
+    }
+  }
   if (CG == 2 && variant == 1)
     return gelu ? launch_tc<256, 6, EPI_BIAS_GELU, 2, 4>(ma, mb, a, max_tiles, st)
                 : launch_tc<256, 6, EPI_BIAS, 2, 4>(ma, mb, a, max_tiles, st);

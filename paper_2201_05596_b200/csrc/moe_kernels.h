@@ -20,11 +20,27 @@ int64_t scan_i64_workspace_elems(int64_t n);
 int launch_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* ws, cudaStream_t st);
 int launch_blelloch_f64(double* tree, int64_t m, cudaStream_t st);
 
-int launch_scatter(const void* x, int64_t S, int64_t row_bytes, int k, int E, int64_t cap,
-                   const int32_t* ids, int32_t* slots, const int32_t* local_rank,
-                   const int32_t* tile_offsets, void* buf, uint8_t* occupied,
-                   const int32_t* slot_base, const int32_t* row_base, int32_t* row_index,
-                   cudaStream_t st);
+struct ScatterArgs {
+  const uint8_t* x = nullptr;        // (S, row_bytes)
+  int64_t S = 0, row_bytes = 0;
+  int k = 1, E = 1;
+  int64_t cap = 0;
+  const int32_t* ids = nullptr;
+  int32_t* slots = nullptr;               // read (API scatter) or written (layer dispatch)
+  const int32_t* local_rank = nullptr;    // non-null: resolve slots from the plan tables
+  const int32_t* tile_offsets = nullptr;
+  uint8_t* buf = nullptr;
+  uint8_t* occupied = nullptr;
+  const int32_t* slot_base = nullptr;     // EP: rank prefix per expert
+  const int32_t* row_base = nullptr;      // EP: send-buffer start row per expert
+  int32_t* row_index = nullptr;           // EP: (S, k) send row or -1
+  const float* gate_probs = nullptr;      // fused combine: (S, k)
+  int32_t* row_token = nullptr;           // fused combine: per buffer row -> token
+  float* row_prob = nullptr;              // fused combine: per buffer row -> gate prob
+  uint8_t* out_dropped = nullptr;         // fused combine: out rows of fully dropped tokens
+};
+
+int launch_scatter(const ScatterArgs& args, cudaStream_t st);
 
 int launch_combine(const void* y, int dtype, int64_t S, int M, int k, int E, int64_t cap,
                    const int32_t* ids, const int32_t* slots, const int32_t* row_index,
@@ -35,7 +51,9 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              int N, const float* bias, void* D, int G, const int32_t* row_start,
                              int64_t row_stride, const int32_t* rows, int64_t rows_const,
                              const int32_t* weight_idx, int64_t max_group_rows, int act,
-                             cudaStream_t st);
+                             cudaStream_t st, const int32_t* row_token = nullptr,
+                             const float* row_prob = nullptr, const void* x_resid = nullptr,
+                             void* out = nullptr);
 
 int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
                           float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,

@@ -267,44 +267,53 @@ __global__ void blelloch_down_kernel(double* tree, int64_t m, int64_t d) {
 // Warp per token: the row is read once and stored to each kept (expert, slot)
 // of the token. With local_rank/tile_offsets given, the slot is resolved here
 // (and written to slots) - the layer path fuses plan_slots into dispatch.
+// For the k=1 fused-combine layer path it also records, per expert-buffer row,
+// the source token and its gate probability (read by the GEMM2 epilogue), and
+// writes out[t] = x[t] for tokens whose every assignment was dropped
+// (arch.py:389: dropped tokens ride the skip connection).
 template <typename V>
-__global__ void scatter_kernel(const uint8_t* __restrict__ x, int64_t S, int64_t row_bytes, int k,
-                               int E, int64_t cap, const int32_t* __restrict__ ids,
-                               int32_t* __restrict__ slots, const int32_t* __restrict__ local_rank,
-                               const int32_t* __restrict__ tile_offsets, uint8_t* __restrict__ buf,
-                               uint8_t* __restrict__ occupied, const int32_t* __restrict__ slot_base,
-                               const int32_t* __restrict__ row_base,
-                               int32_t* __restrict__ row_index) {
+__global__ void scatter_kernel(ScatterArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t nvec = row_bytes / (int64_t)sizeof(V);
-  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
+  const int64_t nvec = a.row_bytes / (int64_t)sizeof(V);
+  const int k = a.k;
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < a.S;
        t += warps_total) {
     int64_t dst0 = -1, dst1 = -1;
     for (int j = 0; j < k; ++j) {
-      const int e = ids[t * k + j];
+      const int e = a.ids[t * k + j];
       int64_t slot;
-      if (local_rank != nullptr) {
-        slot = (int64_t)tile_offsets[(t / kRouteTile) * E + e] + local_rank[t * k + j];
-        if (slot >= cap) slot = -1;
-        if (lane == 0) slots[t * k + j] = (int32_t)slot;
+      if (a.local_rank != nullptr) {
+        slot = (int64_t)a.tile_offsets[(t / kRouteTile) * a.E + e] + a.local_rank[t * k + j];
+        if (slot >= a.cap) slot = -1;
+        if (lane == 0) a.slots[t * k + j] = (int32_t)slot;
       } else {
-        slot = slots[t * k + j];
+        slot = a.slots[t * k + j];
       }
       int64_t d = -1;
       if (slot >= 0) {
         // expert-buffer row e*cap + slot, or (EP send buffer) row_base[e] + slot - slot_base[e]
-        d = row_base != nullptr ? (int64_t)row_base[e] + slot - (slot_base ? slot_base[e] : 0)
-                                : (int64_t)e * cap + slot;
+        d = a.row_base != nullptr
+                ? (int64_t)a.row_base[e] + slot - (a.slot_base ? a.slot_base[e] : 0)
+                : (int64_t)e * a.cap + slot;
         if (j == 0) dst0 = d; else dst1 = d;
-        if (occupied != nullptr && lane == 0) occupied[d] = 1;
+        if (lane == 0) {
+          if (a.occupied != nullptr) a.occupied[d] = 1;
+          if (a.row_token != nullptr) {
+            a.row_token[d] = (int32_t)t;
+            a.row_prob[d] = a.gate_probs[t * k + j];
+          }
+        }
       }
-      if (row_index != nullptr && lane == 0) row_index[t * k + j] = (int32_t)d;
+      if (a.row_index != nullptr && lane == 0) a.row_index[t * k + j] = (int32_t)d;
     }
-    if (dst0 < 0 && dst1 < 0) continue;
-    const V* src = reinterpret_cast<const V*>(x + t * row_bytes);
-    V* d0 = dst0 >= 0 ? reinterpret_cast<V*>(buf + dst0 * row_bytes) : nullptr;
-    V* d1 = dst1 >= 0 ? reinterpret_cast<V*>(buf + dst1 * row_bytes) : nullptr;
+    V* d0 = dst0 >= 0 ? reinterpret_cast<V*>(a.buf + dst0 * a.row_bytes) : nullptr;
+    V* d1 = dst1 >= 0 ? reinterpret_cast<V*>(a.buf + dst1 * a.row_bytes) : nullptr;
+    if (d0 == nullptr && d1 == nullptr) {
+      if (a.out_dropped == nullptr) continue;
+      d0 = reinterpret_cast<V*>(a.out_dropped + t * a.row_bytes);  // out = x
+    }
+    const V* src = reinterpret_cast<const V*>(a.x + t * a.row_bytes);
     constexpr int U = 4;
     int64_t i = lane;
     for (; i + 32 * (U - 1) < nvec; i += 32 * U) {
@@ -519,29 +528,18 @@ int launch_blelloch_f64(double* tree, int64_t m, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
-int launch_scatter(const void* x, int64_t S, int64_t row_bytes, int k, int E, int64_t cap,
-                   const int32_t* ids, int32_t* slots, const int32_t* local_rank,
-                   const int32_t* tile_offsets, void* buf, uint8_t* occupied,
-                   const int32_t* slot_base, const int32_t* row_base, int32_t* row_index,
-                   cudaStream_t st) {
-  if (S == 0) return 0;
+int launch_scatter(const ScatterArgs& args, cudaStream_t st) {
+  if (args.S == 0) return 0;
   const int threads = 256;
-  const int g = grid_for(S, threads / 32, 148 * 64);
-  const uint8_t* xb = (const uint8_t*)x;
-  uint8_t* bb = (uint8_t*)buf;
-#define MOE_SCATTER(V)                                                                        \
-  scatter_kernel<V><<<g, threads, 0, st>>>(xb, S, row_bytes, k, E, cap, ids, slots, local_rank, \
-                                           tile_offsets, bb, occupied, slot_base, row_base,     \
-                                           row_index)
-  if (row_bytes % 16 == 0)
-    MOE_SCATTER(uint4);
-  else if (row_bytes % 8 == 0)
-    MOE_SCATTER(uint2);
-  else if (row_bytes % 4 == 0)
-    MOE_SCATTER(uint32_t);
+  const int g = grid_for(args.S, threads / 32, 148 * 64);
+  if (args.row_bytes % 16 == 0)
+    scatter_kernel<uint4><<<g, threads, 0, st>>>(args);
+  else if (args.row_bytes % 8 == 0)
+    scatter_kernel<uint2><<<g, threads, 0, st>>>(args);
+  else if (args.row_bytes % 4 == 0)
+    scatter_kernel<uint32_t><<<g, threads, 0, st>>>(args);
   else
-    MOE_SCATTER(uint16_t);
-#undef MOE_SCATTER
+    scatter_kernel<uint16_t><<<g, threads, 0, st>>>(args);
   return (int)cudaGetLastError();
 }
 

@@ -61,8 +61,8 @@ def oracle_args(p):
     return experts, shared
 
 
-def run_layer(spec, p, x64, dtype):
-    layer = A.MoeLayer(spec, p, dtype=dtype)
+def run_layer(spec, p, x64, dtype, fuse=True):
+    layer = A.MoeLayer(spec, p, dtype=dtype, fuse_combine=fuse)
     x = torch.as_tensor(x64).to(device="cuda", dtype=dtype)
     logits = torch.empty((x.shape[0], spec.experts), dtype=torch.float32, device="cuda")
     out = layer(x, logits_out=logits)
@@ -121,13 +121,14 @@ def test_golden_layers(dtype):
         close(out.float().cpu().numpy(), want, 2e-2)
 
 
-def test_dropped_tokens_ride_skip_bitwise():
+@pytest.mark.parametrize("fuse", [True, False])
+def test_dropped_tokens_ride_skip_bitwise(fuse):
     # test_arch.py:267-275: capacity 1 per expert, everything else == x exactly
     for dtype in (torch.float32, torch.bfloat16):
         spec = A.LayerSpec(kind="moe", hidden=64, experts=2, gating=GatingConfig(2, 1, 1e-9))
         p = rounded_params(spec, 24, dtype)
         x64 = torch.randn(300, 64, generator=torch.Generator().manual_seed(3)).to(dtype).double().numpy()
-        layer, x, out, logits = run_layer(spec, p, x64, dtype)
+        layer, x, out, logits = run_layer(spec, p, x64, dtype, fuse)
         _, slots = check_routing(layer, logits, spec, 300)
         dropped = (slots < 0).all(axis=1)
         assert dropped.sum() >= 298
@@ -193,6 +194,24 @@ def test_config1_fp32_full():
     ex, sh = oracle_args(p)
     want = O.forward_layer_with_logits(x64, lg, ex, sh, 8, 1, 1.0)
     close(out.cpu().numpy(), want, 1e-5)
+
+
+def test_fused_combine_matches_unfused():
+    """k=1 bf16: the GEMM2-epilogue combine equals the separate combine kernel
+    up to one bf16 rounding of y (the fused path keeps y in fp32)."""
+    S, M, E = 5000, 512, 16
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, 1, 1.0))
+    p = rounded_params(spec, 77, torch.bfloat16)
+    p.gate_w.value[:] += torch.as_tensor(np.random.default_rng(1).normal(0, 0.1, (1, E))).to(
+        torch.bfloat16).double().numpy()
+    x64 = torch.randn(S, M, generator=torch.Generator().manual_seed(5)).to(torch.bfloat16).double().numpy()
+    _, x, out_f, lg_f = run_layer(spec, p, x64, torch.bfloat16, True)
+    lf, _, out_u, lg_u = run_layer(spec, p, x64, torch.bfloat16, False)
+    assert torch.equal(lg_f, lg_u)
+    close(out_f.float().cpu().numpy(), out_u.float().cpu().numpy(), 1e-2)
+    ids, gp, slots, load, cap = lf.plan(S)
+    dropped = (slots < 0).all(dim=1)
+    assert dropped.any() and torch.equal(out_f[dropped], x[dropped])
 
 
 @pytest.mark.parametrize("cfg", [
