@@ -256,6 +256,7 @@ class MoeLayer:
         self.fused_combine = bool(fuse_combine and self.dtype == torch.bfloat16 and
                                   self.k == 1 and self.shared is None)
         self._ws: dict = {}
+        self._pipe = None
 
     # -- workspace -----------------------------------------------------------
     def workspace(self, S: int) -> dict:
@@ -299,10 +300,26 @@ class MoeLayer:
                 logits_out: torch.Tensor | None = None, timer=None) -> torch.Tensor:
         """out = x + combine(experts(dispatch(x))) [+ shared MLP(x)]
         (arch.py:372-392). ``logits_out`` (S, E) fp32 receives the gate logits
-        the routing decided on (the parity tests feed them to the oracle)."""
+        the routing decided on (the parity tests feed them to the oracle).
+
+        A host ``x`` streams through ``pipeline.HostPipeline`` (async H2D /
+        forward / D2H on separate streams, double-buffered); the result is a
+        host tensor valid after the next device synchronisation."""
         if x.dim() != 2 or x.shape[1] != self.M:
             raise ShapeError(f"batch width {tuple(x.shape)} does not match layer hidden {self.M}")
-        if x.device != self.device:  # host input: one H2D copy on the current stream
+        if not x.is_cuda:
+            if self._pipe is None:
+                from .pipeline import HostPipeline
+
+                self._pipe = HostPipeline(self._forward_dev, self.M, self.dtype, self.device)
+            xh = x if x.dtype == self.dtype else x.to(self.dtype)
+            oh = out if (out is not None and not out.is_cuda) else None
+            return self._pipe(xh, oh, logits_out=logits_out, timer=timer)
+        return self._forward_dev(x, out, logits_out, timer)
+
+    def _forward_dev(self, x: torch.Tensor, out: torch.Tensor | None = None,
+                     logits_out: torch.Tensor | None = None, timer=None) -> torch.Tensor:
+        if x.device != self.device:
             x = x.to(device=self.device, non_blocking=True)
         if x.dtype != self.dtype:
             x = x.to(self.dtype)

@@ -146,6 +146,7 @@ class EPMoeLayer:
             self.b2[i] = _t(p.b2, dev, torch.float32).reshape(M)
         self.shared = DenseFfn(shared, M, dtype, dev) if spec.residual else None
         self._ws: dict = {}
+        self._pipe = None
         self.last_plan: ExchangePlan | None = None
 
     @classmethod
@@ -218,7 +219,18 @@ class EPMoeLayer:
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, timer=None):
         """out = x + combine(experts(dispatch(x))) [+ shared(x)] for this rank's
-        tokens, experts evaluated on their owner ranks."""
+        tokens, experts evaluated on their owner ranks. Host inputs stream
+        through ``pipeline.HostPipeline`` like ``MoeLayer``."""
+        if not x.is_cuda:
+            if self._pipe is None:
+                from .pipeline import HostPipeline
+
+                self._pipe = HostPipeline(self._forward_dev, self.M, self.dtype, self.dev)
+            oh = out if (out is not None and not out.is_cuda) else None
+            return self._pipe(x.to(self.dtype), oh, timer=timer)
+        return self._forward_dev(x, out, timer)
+
+    def _forward_dev(self, x: torch.Tensor, out: torch.Tensor | None = None, timer=None):
         if x.device != self.dev:
             x = x.to(self.dev, non_blocking=True)
         x = x.to(self.dtype).contiguous()

@@ -1,0 +1,76 @@
+"""Host <-> device streaming for layers called with host tensors.
+
+A layer called with a (pinned) host batch copies it in on an H2D stream into
+one of two device staging buffers, runs the forward on the caller's stream,
+and copies the result out on a D2H stream from one of two device output
+buffers. With two slots, step i+1's upload and step i-1's download overlap
+step i's kernels (the copy engines of each direction are separate), so a
+stream of batches runs at max(H2D, compute, D2H) per batch instead of their
+sum. Every call is asynchronous; results are valid once the caller syncs
+(``torch.cuda.synchronize()`` or ``HostPipeline.wait()``).
+"""
+
+from __future__ import annotations
+
+import torch
+
+
+class HostPipeline:
+    def __init__(self, fn, width: int, dtype: torch.dtype, device) -> None:
+        self.fn, self.width, self.dtype, self.device = fn, width, dtype, device
+        self.h2d = torch.cuda.Stream(device=device)
+        self.d2h = torch.cuda.Stream(device=device)
+        self.rows = -1
+        self.slot = 0
+        self.x_dev = [None, None]
+        self.y_dev = [None, None]
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]       # upload into slot done
+        self.ev_used = [torch.cuda.Event() for _ in range(2)]     # compute reading slot done
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]      # download from slot done
+        self.started = [False, False]
+
+    def _alloc(self, rows: int) -> None:
+        if rows == self.rows:
+            return
+        torch.cuda.current_stream(self.device).synchronize()
+        self.x_dev = [torch.empty((rows, self.width), dtype=self.dtype, device=self.device)
+                      for _ in range(2)]
+        self.y_dev = [torch.empty((rows, self.width), dtype=self.dtype, device=self.device)
+                      for _ in range(2)]
+        self.rows = rows
+        self.started = [False, False]
+
+    def __call__(self, x_host: torch.Tensor, out_host: torch.Tensor | None = None, **kw):
+        rows = x_host.shape[0]
+        self._alloc(rows)
+        j = self.slot
+        self.slot ^= 1
+        cur = torch.cuda.current_stream(self.device)
+        if out_host is None:
+            out_host = torch.empty((rows, self.width), dtype=self.dtype, pin_memory=True)
+        # upload: the staging slot must no longer be read by the previous forward
+        if self.started[j]:
+            self.h2d.wait_event(self.ev_used[j])
+        with torch.cuda.stream(self.h2d):
+            self.x_dev[j].copy_(x_host, non_blocking=True)
+            self.ev_in[j].record(self.h2d)
+        # compute: needs the upload, and the output slot must be downloaded already
+        cur.wait_event(self.ev_in[j])
+        if self.started[j]:
+            cur.wait_event(self.ev_out[j])
+        self.fn(self.x_dev[j], out=self.y_dev[j], **kw)
+        self.ev_used[j].record(cur)
+        # download
+        self.d2h.wait_event(self.ev_used[j])
+        with torch.cuda.stream(self.d2h):
+            out_host.copy_(self.y_dev[j], non_blocking=True)
+            self.ev_out[j].record(self.d2h)
+        self.started[j] = True
+        return out_host
+
+    def wait(self) -> None:
+        """Make the caller's stream wait for every outstanding download."""
+        cur = torch.cuda.current_stream(self.device)
+        for j in range(2):
+            if self.started[j]:
+                cur.wait_event(self.ev_out[j])

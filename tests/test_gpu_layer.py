@@ -275,3 +275,22 @@ def test_config3_routing_full_and_sampled_outputs():
     dropped = (slots < 0).all(axis=1)
     d = torch.as_tensor(dropped, device=dev)
     assert torch.equal(out[d], x[d])
+
+
+def test_host_pipeline_matches_device_forward():
+    """Host-tensor calls stream through HostPipeline: same results as the
+    device call, for several back-to-back batches with alternating outputs."""
+    S, M, E = 3000, 256, 8
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=True,
+                       gating=GatingConfig(E, 2, 1.0))
+    p = rounded_params(spec, 3, torch.bfloat16)
+    layer = A.MoeLayer(spec, p, dtype=torch.bfloat16)
+    xs = [torch.randn(S, M, generator=torch.Generator().manual_seed(i)).to(torch.bfloat16).pin_memory()
+          for i in range(4)]
+    outs = [torch.empty(S, M, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+    for xh, oh in zip(xs, outs):
+        layer(xh, out=oh)
+    torch.cuda.synchronize()
+    for xh, oh in zip(xs, outs):
+        want = layer(xh.cuda()).cpu()
+        assert torch.equal(oh, want)
