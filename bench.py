@@ -268,7 +268,7 @@ def run_gpu(args):
         return
     hbm, tf_burst, tf_sus, src = peaks()
     # dominant kernel: the grouped expert GEMM (GEMM1 + GEMM2 launches)
-    gemm_ms = phases.get("gemm1", 0.0) + phases.get("gemm2", 0.0)
+    gemm_ms = sum(v for kk, v in phases.items() if kk.startswith("gemm"))
     kept_rank = kept_total / world
     flops = 4.0 * kept_rank * M * F  # 2*A*M*F per GEMM launch, two launches
     achieved = flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None

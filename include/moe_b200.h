@@ -166,6 +166,67 @@ int moe_grouped_gemm_f32(const float* A, int K, const float* B, int N, const flo
                          const int32_t* rows, int64_t rows_const, const int32_t* weight_idx,
                          int64_t max_group_rows, int act, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Expert parallelism over NVLink peer memory (one process per GPU of a box).
+ * Replaces the two all-to-alls of the EP layer (new; placement after
+ * planner.py:101-109, delivery order of commsim.py:188-189) with stores fused
+ * into the dispatch kernel and the GEMM2 epilogue.
+ * ------------------------------------------------------------------------- */
+
+/* Device memory shareable with the other ranks' processes (cudaMalloc +
+ * cudaIpc handles; 64-byte handles, exchanged by the caller). Zero-filled. */
+int moe_ipc_malloc(size_t bytes, void** ptr);
+int moe_ipc_free(void* ptr);
+int moe_ipc_get_handle(void* ptr, void* handle64);
+int moe_ipc_open_handle(const void* handle64, void** ptr);
+int moe_ipc_close_handle(void* ptr);
+
+/* Global-capacity exchange plan on device from the all-gathered counts
+ * (world, E) int32: slot_base (E) = assignments to e on lower ranks;
+ * row_base (E) = first row of this rank's rows for e in the owner's receive
+ * buffer, laid out [local expert][global slot] (sources in rank order, i.e.
+ * the single-GPU expert buffer without padding); as an owner, seg_start /
+ * seg_rows (E/world) per local expert and recv_rows (1). */
+int moe_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap, int32_t* slot_base,
+                int32_t* row_base, int32_t* seg_start, int32_t* seg_rows, int32_t* recv_rows,
+                void* stream);
+
+/* System-scope flag barrier over peer signal pads: writes `epoch` into slot
+ * [rank] of every peer's pad (peer_signal: device array of world pointers)
+ * and waits until my_signal[i] >= epoch for all i. Bounded: sets
+ * *error_flag = 1 after ~10 s instead of hanging. */
+int moe_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank, int epoch,
+                    int* error_flag, void* stream);
+
+/* Dispatch straight into the owners' receive buffers over NVLink: kept row
+ * (t, j) of expert e goes to peer_recv[e / e_per_rank] at row
+ * row_base[e] + slot - slot_base[e], with its token index and gate
+ * probability to peer_token / peer_prob (device arrays of world pointers);
+ * row_index (S, k) gets that owner-side row (or -1). Fully dropped tokens:
+ * out_dropped[t] = x[t] (local). */
+int moe_dispatch_p2p(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                     const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                     const float* gate_probs, const int32_t* slot_base, const int32_t* row_base,
+                     int e_per_rank, void* const* peer_recv, int32_t* const* peer_token,
+                     float* const* peer_prob, int32_t* slots, int32_t* row_index,
+                     void* out_dropped, void* stream);
+
+/* Owner side of a k=1 EP layer: GEMM2 + combine + residual, in the receive
+ * layout: out_rows[r] = x_rows[r] + row_prob[r] * (A[r] @ B_w^T + b_w), with
+ * x_rows = the dispatched token rows (GEMM1's input). */
+int moe_grouped_gemm_bf16_combine_rows(const void* A, int64_t a_rows, int K, const void* B,
+                                       int64_t b_rows, int N, const float* bias, int num_groups,
+                                       const int32_t* row_start, const int32_t* rows,
+                                       const int32_t* weight_idx, int64_t max_group_rows,
+                                       const int32_t* row_token, const float* row_prob,
+                                       const void* x_rows, void* out_rows, void* stream);
+
+/* Source side (k=1): out[t] = peer_rows[owner(ids[t])][row_index[t]] over
+ * NVLink for every kept token (peer_rows: device array of world pointers). */
+int moe_pull_rows_p2p(int64_t S, int64_t row_bytes, int E, int k, const int32_t* ids,
+                      const int32_t* row_index, int e_per_rank, void* const* peer_rows, void* out,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

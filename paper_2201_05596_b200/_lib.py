@@ -48,6 +48,18 @@ SIGNATURES = {
                                    _I, _P]),
     "moe_grouped_gemm_bf16_combine": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _L, _P, _L, _P,
                                            _L, _P, _P, _P, _P, _P]),
+    "moe_ipc_malloc": (_I, [_Z, _P]),
+    "moe_ipc_free": (_I, [_P]),
+    "moe_ipc_get_handle": (_I, [_P, _P]),
+    "moe_ipc_open_handle": (_I, [_P, _P]),
+    "moe_ipc_close_handle": (_I, [_P]),
+    "moe_ep_plan": (_I, [_P, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
+    "moe_ipc_barrier": (_I, [_P, _P, _I, _I, _I, _P, _P]),
+    "moe_dispatch_p2p": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P,
+                              _P, _P, _P]),
+    "moe_grouped_gemm_bf16_combine_rows": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _P, _P, _L,
+                                                _P, _P, _P, _P, _P]),
+    "moe_pull_rows_p2p": (_I, [_L, _L, _I, _I, _P, _P, _I, _P, _P, _P]),
     "moe_grouped_gemm_f32": (_I, [_P, _I, _P, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L, _I, _P]),
 }
 
@@ -127,7 +139,9 @@ def dtype_code(dt: torch.dtype) -> int:
 # instrumentation: kernel-launch counter and per-phase CUDA-event timer
 # ---------------------------------------------------------------------------
 
-_NON_LAUNCH = {"moe_abi_version", "moe_plan_workspace_bytes", "moe_scan_workspace_bytes"}
+_NON_LAUNCH = {"moe_abi_version", "moe_plan_workspace_bytes", "moe_scan_workspace_bytes",
+               "moe_ipc_malloc", "moe_ipc_free", "moe_ipc_get_handle", "moe_ipc_open_handle",
+               "moe_ipc_close_handle"}
 # entry points that launch more than one kernel per call
 _MULTI = {"moe_build_plan": 3}
 _launches = 0

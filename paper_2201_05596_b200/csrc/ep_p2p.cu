@@ -1,0 +1,253 @@
+// Expert parallelism over NVLink peer memory (one process per GPU, one box).
+//
+//   * moe_ipc_*      : cudaMalloc'd regions shared between the ranks' processes
+//                      (cudaIpc handles exchanged by the caller over NCCL)
+//   * ep_plan_kernel : from the all-gathered (world, E) expert counts, the
+//                      global-capacity exchange plan on device (no host sync):
+//                      this rank's slot prefix per expert, where its rows land
+//                      in each owner's receive buffer, and (as an owner) the
+//                      per-local-expert row ranges of its own receive buffer
+//   * ipc_barrier    : a system-scope release/acquire flag exchange between the
+//                      ranks (bounded spin: sets an error flag after ~10 s
+//                      instead of hanging)
+// The data movement is fused into the kernels around the GEMMs: the dispatch
+// kernel stores token rows straight into the owners' receive buffers; the owner's
+// GEMM2 epilogue combines (x + p*y) in place in its receive layout, and the
+// source pulls its rows back with wide NVLink loads (pull_rows_kernel).
+#include "common.cuh"
+#include "moe_kernels.h"
+
+#include <string.h>
+
+namespace moe {
+
+__global__ void ep_plan_kernel(const int32_t* __restrict__ counts, int world, int rank, int E,
+                               int64_t cap, int32_t* __restrict__ slot_base,
+                               int32_t* __restrict__ row_base, int32_t* __restrict__ seg_start,
+                               int32_t* __restrict__ seg_rows, int32_t* __restrict__ recv_rows) {
+  extern __shared__ int kept[];  // [world][E]
+  const int e_loc = E / world;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int64_t base = 0;  // assignments to e on lower ranks: the global slot of my first one
+    for (int s = 0; s < world; ++s) {
+      const int c = counts[s * E + e];
+      int64_t kp = cap - base;
+      kp = kp < 0 ? 0 : (kp > c ? c : kp);
+      kept[s * E + e] = (int)kp;
+      if (s == rank) slot_base[e] = (int)base;
+      base += c;
+    }
+  }
+  __syncthreads();
+  // owner o's receive buffer is expert-major: [local expert j][source s][rows in
+  // slot order] = [local expert][global slot], i.e. the single-GPU expert buffer
+  // without padding. My rows for expert e start at
+  //   sum_{j' < e % e_loc} sum_s kept[s][o*e_loc + j']  +  sum_{s < rank} kept[s][e]
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int o = e / e_loc, el = e % e_loc;
+    int64_t st = 0;
+    for (int j = 0; j < el; ++j)
+      for (int s = 0; s < world; ++s) st += kept[s * E + o * e_loc + j];
+    for (int s = 0; s < rank; ++s) st += kept[s * E + e];
+    row_base[e] = (int)st;
+  }
+  if (threadIdx.x == 0) {  // as an owner: one group per local expert
+    int64_t run = 0;
+    for (int j = 0; j < e_loc; ++j) {
+      int64_t r = 0;
+      for (int s = 0; s < world; ++s) r += kept[s * E + rank * e_loc + j];
+      seg_start[j] = (int)run;
+      seg_rows[j] = (int)r;
+      run += r;
+    }
+    *recv_rows = (int)run;
+  }
+}
+
+__global__ void ipc_barrier_kernel(int* const* __restrict__ peer_signal, int* my_signal, int world,
+                                   int rank, int epoch, int* error_flag) {
+  const int i = threadIdx.x;
+  if (i >= world) return;
+  int* dst = peer_signal[i] + rank;
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(dst), "r"(epoch) : "memory");
+  const long long t0 = clock64();
+  while (true) {
+    int v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(my_signal + i) : "memory");
+    if (v >= epoch) break;
+    if (clock64() - t0 > 20000000000LL) {  // ~10 s: report instead of hanging the GPU
+      atomicExch(error_flag, 1);
+      break;
+    }
+    __nanosleep(64);
+  }
+}
+
+// Source side of the return (k=1): out[t] = owner's combined row, loaded over
+// NVLink from the owner's receive-layout buffer (16 B per lane, 512 B per warp
+// access). Dropped tokens were already written (out = x) by the dispatch.
+template <typename V>
+__global__ void pull_rows_kernel(int64_t S, int64_t row_bytes, int k, int e_per_rank,
+                                 const int32_t* __restrict__ ids,
+                                 const int32_t* __restrict__ row_index,
+                                 uint8_t* const* __restrict__ peer_rows, uint8_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t nvec = row_bytes / (int64_t)sizeof(V);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
+       t += warps_total) {
+    const int32_t r = row_index[t * k];
+    if (r < 0) continue;
+    const V* src = reinterpret_cast<const V*>(peer_rows[ids[t * k] / e_per_rank] +
+                                              (int64_t)r * row_bytes);
+    V* dst = reinterpret_cast<V*>(out + t * row_bytes);
+    constexpr int U = 4;
+    int64_t i = lane;
+    for (; i + 32 * (U - 1) < nvec; i += 32 * U) {
+      V v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = src[i + 32 * u];
+#pragma unroll
+      for (int u = 0; u < U; ++u) dst[i + 32 * u] = v[u];
+    }
+    for (; i < nvec; i += 32) dst[i] = src[i];
+  }
+}
+
+int launch_pull_rows(int64_t S, int64_t row_bytes, int k, int e_per_rank, const int32_t* ids,
+                     const int32_t* row_index, uint8_t* const* peer_rows, uint8_t* out,
+                     cudaStream_t st) {
+  if (S == 0) return 0;
+  int64_t g = (S + 7) / 8;
+  if (g > 148 * 64) g = 148 * 64;
+  if (row_bytes % 16 == 0)
+    pull_rows_kernel<uint4><<<(unsigned)g, 256, 0, st>>>(S, row_bytes, k, e_per_rank, ids,
+                                                         row_index, peer_rows, out);
+  else
+    pull_rows_kernel<uint16_t><<<(unsigned)g, 256, 0, st>>>(S, row_bytes, k, e_per_rank, ids,
+                                                            row_index, peer_rows, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap,
+                   int32_t* slot_base, int32_t* row_base, int32_t* seg_start, int32_t* seg_rows,
+                   int32_t* recv_rows, cudaStream_t st) {
+  const size_t smem = (size_t)world * E * sizeof(int);
+  if (smem > 48 * 1024) return MOE_EINVAL;
+  ep_plan_kernel<<<1, 256, smem, st>>>(counts, world, rank, E, cap, slot_base, row_base, seg_start,
+                                       seg_rows, recv_rows);
+  return (int)cudaGetLastError();
+}
+
+int launch_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank, int epoch,
+                       int* error_flag, cudaStream_t st) {
+  ipc_barrier_kernel<<<1, 32, 0, st>>>(peer_signal, my_signal, world, rank, epoch, error_flag);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace moe
+
+#define CHECK(cond)                 \
+  do {                              \
+    if (!(cond)) return MOE_EINVAL; \
+  } while (0)
+
+extern "C" {
+
+int moe_ipc_malloc(size_t bytes, void** ptr) {
+  CHECK(ptr && bytes > 0);
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaMemset(*ptr, 0, bytes);
+}
+
+int moe_ipc_free(void* ptr) { return ptr ? (int)cudaFree(ptr) : MOE_OK; }
+
+int moe_ipc_get_handle(void* ptr, void* handle64) {
+  CHECK(ptr && handle64);
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e != cudaSuccess) return (int)e;
+  memcpy(handle64, &h, sizeof(h));
+  return MOE_OK;
+}
+
+int moe_ipc_open_handle(const void* handle64, void** ptr) {
+  CHECK(ptr && handle64);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  return (int)cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+}
+
+int moe_ipc_close_handle(void* ptr) { return ptr ? (int)cudaIpcCloseMemHandle(ptr) : MOE_OK; }
+
+int moe_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap, int32_t* slot_base,
+                int32_t* row_base, int32_t* seg_start, int32_t* seg_rows, int32_t* recv_rows,
+                void* stream) {
+  CHECK(world >= 1 && rank >= 0 && rank < world && E >= world && E % world == 0 && cap >= 0);
+  CHECK(counts && slot_base && row_base && seg_start && seg_rows && recv_rows);
+  return moe::launch_ep_plan(counts, world, rank, E, cap, slot_base, row_base, seg_start, seg_rows,
+                             recv_rows, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int moe_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank, int epoch,
+                    int* error_flag, void* stream) {
+  CHECK(world >= 1 && world <= 32 && rank >= 0 && rank < world && epoch > 0);
+  CHECK(peer_signal && my_signal && error_flag);
+  return moe::launch_ipc_barrier(peer_signal, my_signal, world, rank, epoch, error_flag,
+                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+int moe_dispatch_p2p(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
+                     const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
+                     const float* gate_probs, const int32_t* slot_base, const int32_t* row_base,
+                     int e_per_rank, void* const* peer_recv, int32_t* const* peer_token,
+                     float* const* peer_prob, int32_t* slots, int32_t* row_index,
+                     void* out_dropped, void* stream) {
+  CHECK(S >= 0 && row_bytes >= 0 && row_bytes % 2 == 0 && E >= 1 && (k == 1 || k == 2) &&
+        cap >= 0 && e_per_rank >= 1);
+  if (S == 0) return MOE_OK;
+  CHECK(x && ids && local_rank && tile_offsets && gate_probs && slot_base && row_base &&
+        peer_recv && peer_token && peer_prob && slots && row_index);
+  moe::ScatterArgs a;
+  a.x = static_cast<const uint8_t*>(x);
+  a.S = S, a.row_bytes = row_bytes, a.k = k, a.E = E, a.cap = cap;
+  a.ids = ids, a.slots = slots, a.local_rank = local_rank, a.tile_offsets = tile_offsets;
+  a.gate_probs = gate_probs;
+  a.slot_base = slot_base, a.row_base = row_base;
+  a.peer_buf = reinterpret_cast<uint8_t* const*>(peer_recv);
+  a.peer_token = peer_token, a.peer_prob = peer_prob, a.e_per_rank = e_per_rank;
+  a.out_dropped = static_cast<uint8_t*>(out_dropped);
+  a.row_index = row_index;
+  return moe::launch_scatter(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int moe_pull_rows_p2p(int64_t S, int64_t row_bytes, int E, int k, const int32_t* ids,
+                      const int32_t* row_index, int e_per_rank, void* const* peer_rows, void* out,
+                      void* stream) {
+  CHECK(S >= 0 && row_bytes >= 0 && row_bytes % 2 == 0 && E >= 1 && k == 1 && e_per_rank >= 1);
+  if (S == 0) return MOE_OK;
+  CHECK(ids && row_index && peer_rows && out);
+  return moe::launch_pull_rows(S, row_bytes, k, e_per_rank, ids, row_index,
+                               reinterpret_cast<uint8_t* const*>(peer_rows),
+                               static_cast<uint8_t*>(out), reinterpret_cast<cudaStream_t>(stream));
+}
+
+int moe_grouped_gemm_bf16_combine_rows(const void* A, int64_t a_rows, int K, const void* B,
+                                       int64_t b_rows, int N, const float* bias, int num_groups,
+                                       const int32_t* row_start, const int32_t* rows,
+                                       const int32_t* weight_idx, int64_t max_group_rows,
+                                      const int32_t* row_token, const float* row_prob,
+                                      const void* x_rows, void* out_rows, void* stream) {
+  CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1);
+  CHECK(max_group_rows >= 0);
+  if (a_rows == 0 || max_group_rows == 0) return MOE_OK;
+  CHECK(A && B && row_start && rows && row_token && row_prob && x_rows && out_rows);
+  return moe::launch_grouped_gemm_bf16(A, a_rows, K, B, b_rows, N, bias, nullptr, num_groups,
+                                       row_start, 0, rows, 0, weight_idx, max_group_rows, 2,
+                                       reinterpret_cast<cudaStream_t>(stream), row_token, row_prob,
+                                       x_rows, out_rows, 1);
+}
+
+}  // extern "C"

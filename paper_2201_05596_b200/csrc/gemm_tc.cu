@@ -63,8 +63,12 @@ struct GemmArgs {
   // fused combine epilogue
   const int32_t* row_token;   // [a_rows] token of each expert-buffer row
   const float* row_prob;      // [a_rows] its gate probability
-  const __nv_bfloat16* x_resid;  // [S, N]
+  const __nv_bfloat16* x_resid;  // [S, N] indexed by token, or [a_rows, N] by row (x_by_row)
   __nv_bfloat16* out;            // [S, N]
+  // EP owner side: the residual x is the (dispatched) row itself and the combined
+  // row is stored at the same row of `out` (receive layout); the source rank then
+  // pulls it over NVLink
+  int x_by_row;
 };
 
 // CG = 1: one CTA computes a BM x BN tile (tcgen05.mma.cta_group::1, M=128).
@@ -303,8 +307,8 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
         if constexpr (EPI == EPI_BIAS_COMBINE) {
           const int64_t tok = valid ? args.row_token[out_row] : 0;
           prob = valid ? args.row_prob[out_row] : 0.f;
-          drow = args.out + tok * N;
-          xrow = args.x_resid + tok * N;
+          drow = args.out + (args.x_by_row ? out_row : tok) * N;
+          xrow = args.x_resid + (args.x_by_row ? out_row : tok) * N;
         }
         // TMEM loads double-buffered across 32-column chunks: the load of
         // chunk c+1 is in flight while chunk c is biased, activated and stored.
@@ -569,7 +573,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              int64_t row_stride, const int32_t* rows, int64_t rows_const,
                              const int32_t* weight_idx, int64_t max_group_rows, int act,
                              cudaStream_t st, const int32_t* row_token, const float* row_prob,
-                             const void* x_resid, void* out) {
+                             const void* x_resid, void* out, int x_by_row) {
   if (G < 1 || G > kMaxGroups || K < 1 || N < 1 || (K % 8) != 0) return MOE_EINVAL;
   int BN = 256;
   if (N <= 32) BN = 32;
@@ -604,6 +608,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.row_prob = row_prob;
   a.x_resid = (const __nv_bfloat16*)x_resid;
   a.out = (__nv_bfloat16*)out;
+  a.x_by_row = x_by_row;
   const int64_t nblk = (N + BN - 1) / BN;
   const int64_t tm = (int64_t)BM * CG;
   const int64_t max_tiles = (int64_t)G * ((max_group_rows + tm - 1) / tm) * nblk;

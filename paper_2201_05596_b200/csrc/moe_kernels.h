@@ -38,6 +38,12 @@ struct ScatterArgs {
   int32_t* row_token = nullptr;           // fused combine: per buffer row -> token
   float* row_prob = nullptr;              // fused combine: per buffer row -> gate prob
   uint8_t* out_dropped = nullptr;         // fused combine: out rows of fully dropped tokens
+  // EP over NVLink peer memory: per-rank receive buffer / row_token / row_prob bases
+  // (device arrays of `world` pointers); owner of expert e = e / e_per_rank
+  uint8_t* const* peer_buf = nullptr;
+  int32_t* const* peer_token = nullptr;
+  float* const* peer_prob = nullptr;
+  int e_per_rank = 1;
 };
 
 int launch_scatter(const ScatterArgs& args, cudaStream_t st);
@@ -53,7 +59,17 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              const int32_t* weight_idx, int64_t max_group_rows, int act,
                              cudaStream_t st, const int32_t* row_token = nullptr,
                              const float* row_prob = nullptr, const void* x_resid = nullptr,
-                             void* out = nullptr);
+                             void* out = nullptr, int x_by_row = 0);
+
+// expert parallelism over NVLink peer memory (ep_p2p.cu)
+int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap,
+                   int32_t* slot_base, int32_t* row_base, int32_t* seg_start, int32_t* seg_rows,
+                   int32_t* recv_rows, cudaStream_t st);
+int launch_pull_rows(int64_t S, int64_t row_bytes, int k, int e_per_rank, const int32_t* ids,
+                     const int32_t* row_index, uint8_t* const* peer_rows, uint8_t* out,
+                     cudaStream_t st);
+int launch_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank, int epoch,
+                       int* error_flag, cudaStream_t st);
 
 int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
                           float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,

@@ -280,6 +280,8 @@ __global__ void scatter_kernel(ScatterArgs a) {
   for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < a.S;
        t += warps_total) {
     int64_t dst0 = -1, dst1 = -1;
+    uint8_t* base0 = a.buf;
+    uint8_t* base1 = a.buf;
     for (int j = 0; j < k; ++j) {
       const int e = a.ids[t * k + j];
       int64_t slot;
@@ -296,19 +298,28 @@ __global__ void scatter_kernel(ScatterArgs a) {
         d = a.row_base != nullptr
                 ? (int64_t)a.row_base[e] + slot - (a.slot_base ? a.slot_base[e] : 0)
                 : (int64_t)e * a.cap + slot;
-        if (j == 0) dst0 = d; else dst1 = d;
+        uint8_t* base = a.buf;
+        int32_t* rtok = a.row_token;
+        float* rprob = a.row_prob;
+        if (a.peer_buf != nullptr) {  // EP over NVLink: the owner rank's receive buffer
+          const int owner = e / a.e_per_rank;
+          base = a.peer_buf[owner];
+          rtok = a.peer_token[owner];
+          rprob = a.peer_prob[owner];
+        }
+        if (j == 0) { dst0 = d; base0 = base; } else { dst1 = d; base1 = base; }
         if (lane == 0) {
           if (a.occupied != nullptr) a.occupied[d] = 1;
-          if (a.row_token != nullptr) {
-            a.row_token[d] = (int32_t)t;
-            a.row_prob[d] = a.gate_probs[t * k + j];
+          if (rtok != nullptr) {
+            rtok[d] = (int32_t)t;
+            rprob[d] = a.gate_probs[t * k + j];
           }
         }
       }
       if (a.row_index != nullptr && lane == 0) a.row_index[t * k + j] = (int32_t)d;
     }
-    V* d0 = dst0 >= 0 ? reinterpret_cast<V*>(a.buf + dst0 * a.row_bytes) : nullptr;
-    V* d1 = dst1 >= 0 ? reinterpret_cast<V*>(a.buf + dst1 * a.row_bytes) : nullptr;
+    V* d0 = dst0 >= 0 ? reinterpret_cast<V*>(base0 + dst0 * a.row_bytes) : nullptr;
+    V* d1 = dst1 >= 0 ? reinterpret_cast<V*>(base1 + dst1 * a.row_bytes) : nullptr;
     if (d0 == nullptr && d1 == nullptr) {
       if (a.out_dropped == nullptr) continue;
       d0 = reinterpret_cast<V*>(a.out_dropped + t * a.row_bytes);  // out = x
@@ -332,6 +343,8 @@ __global__ void scatter_kernel(ScatterArgs a) {
       if (d1) d1[i] = r;
     }
   }
+  // peer stores must be performed (acknowledged) before the barrier kernel signals
+  if (a.peer_buf != nullptr) __threadfence_system();
 }
 
 // ============================================================ combine

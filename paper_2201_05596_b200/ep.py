@@ -13,7 +13,15 @@ its own shard). One all-gather of the per-rank (E,) expert counts gives every
 rank those prefixes, so routing, slots and the dropped set are bit-identical
 to ``build_dispatch_plan`` run on the whole batch at any p.
 
-Exchange (one NCCL all-to-all each way over NVLink):
+Two transports. "p2p" (k=1 layers, default): no collective on the data path -
+the dispatch kernel stores each kept row straight into its owner's receive
+buffer over NVLink (laid out [local expert][global slot], i.e. the single-GPU
+expert buffer), the owner's GEMM2 epilogue combines in place (x + p*y), and
+the source pulls its rows back with wide NVLink loads; a 2-line flag barrier
+(system-scope release/acquire) separates the phases, and the plan is computed
+on device from the all-gathered counts (no host sync).
+
+"nccl" (any k, shared MLP) - one NCCL all-to-all each way:
   send buffer on rank r : kept rows ordered (owner rank, expert, slot)
   receive buffer        : [source rank][local expert][rows in slot order]
                           (commsim's delivery contract: ordered by source,
@@ -113,7 +121,7 @@ class EPMoeLayer:
     """One MoE layer sharded over the ranks of ``group`` (bf16, tcgen05 path)."""
 
     def __init__(self, spec: LayerSpec, gate_w, local_experts, shared=None, group=None,
-                 dtype=torch.bfloat16, device=None) -> None:
+                 dtype=torch.bfloat16, device=None, transport: str = "auto") -> None:
         if spec.kind != "moe":
             raise ShapeError("EPMoeLayer needs a moe LayerSpec")
         if dtype != torch.bfloat16:
@@ -145,7 +153,20 @@ class EPMoeLayer:
             self.b1[i] = _t(p.b1, dev, torch.float32).reshape(F)
             self.b2[i] = _t(p.b2, dev, torch.float32).reshape(M)
         self.shared = DenseFfn(shared, M, dtype, dev) if spec.residual else None
+        # "p2p": dispatch stores rows into the owners' receive buffers and the GEMM2
+        # epilogue stores combined rows into the sources' outputs, over NVLink peer
+        # memory (k=1, no shared MLP); "nccl": two all_to_all_single exchanges.
+        p2p_ok = self.k == 1 and self.shared is None
+        if transport == "auto":
+            transport = "p2p" if p2p_ok else "nccl"
+        if transport == "p2p" and not p2p_ok:
+            raise ValueError("the peer-memory transport covers k=1 layers without a shared MLP")
+        if transport not in ("p2p", "nccl"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
         self._ws: dict = {}
+        self._p2p: dict | None = None
+        self._epoch = 0
         self._pipe = None
         self.last_plan: ExchangePlan | None = None
 
@@ -231,6 +252,8 @@ class EPMoeLayer:
         return self._forward_dev(x, out, timer)
 
     def _forward_dev(self, x: torch.Tensor, out: torch.Tensor | None = None, timer=None):
+        if self.transport == "p2p":
+            return self._forward_p2p(x, out, timer)
         if x.device != self.dev:
             x = x.to(self.dev, non_blocking=True)
         x = x.to(self.dtype).contiguous()
@@ -308,8 +331,145 @@ class EPMoeLayer:
         return out
 
     def kept_assignments(self, S: int) -> int:
+        if self.transport == "p2p":
+            return int(self._ws[S]["kept"].sum().item())
         return int(self.last_plan.kept[self.rank].sum()) if self.last_plan is not None else 0
 
+    # ------------------------------------------------------------------ p2p
+    def _p2p_state(self, S: int) -> dict:
+        st = self._p2p
+        if st is not None and st["S"] == S:
+            return st
+        if st is not None:
+            st["region"].close()
+        # the peer-memory layout is sized from the global batch: all ranks equal S
+        sizes = torch.tensor([S], dtype=torch.int64, device=self.dev)
+        alls = torch.empty(self.world, dtype=torch.int64, device=self.dev)
+        dist.all_gather_into_tensor(alls, sizes, group=self.group)
+        if int(alls.min()) != int(alls.max()):
+            raise ValueError("the peer-memory transport needs the same token count on every rank")
+        from .ipc import IpcRegion
+
+        M, k = self.M, self.k
+        cap = self.spec.gating.capacity(S * self.world)
+        rmax = max(self.E_loc * cap, 1)
+
+        def al(n):
+            return (n + 255) // 256 * 256
+
+        off_recv = 0
+        off_tok = off_recv + al(rmax * M * 2)
+        off_prob = off_tok + al(rmax * 4)
+        off_ret = off_prob + al(rmax * 4)
+        off_sig = off_ret + al(rmax * M * 2)
+        total = off_sig + al(64 * 4)
+        region = IpcRegion(total, self.group, self.dev)
+        i32 = dict(dtype=torch.int32, device=self.dev)
+        G = self.E_loc
+        st = dict(
+            S=S, cap=cap, rmax=rmax, region=region,
+            recv=region.tensor(off_recv, (rmax, M), torch.bfloat16),
+            row_token=region.tensor(off_tok, (rmax,), torch.int32),
+            row_prob=region.tensor(off_prob, (rmax,), torch.float32),
+            ret=region.tensor(off_ret, (rmax, M), torch.bfloat16),
+            signal=region.tensor(off_sig, (64,), torch.int32),
+            peer_recv=region.ptr_table(off_recv), peer_tok=region.ptr_table(off_tok),
+            peer_prob=region.ptr_table(off_prob), peer_ret=region.ptr_table(off_ret),
+            peer_sig=region.ptr_table(off_sig),
+            slot_base=torch.empty(self.E, **i32), row_base=torch.empty(self.E, **i32),
+            seg_start=torch.empty(G, **i32), seg_rows=torch.empty(G, **i32),
+            seg_w=torch.arange(G, **i32), recv_rows=torch.empty(1, **i32),
+            h=torch.empty((rmax, self.F), dtype=self.dtype, device=self.dev),
+            err=torch.zeros(1, **i32),
+        )
+        dist.barrier(group=self.group)
+        self._p2p = st
+        return st
+
+    def _barrier(self, st: dict) -> None:
+        self._epoch += 1
+        _lib.call("moe_ipc_barrier", st["peer_sig"].data_ptr(), st["signal"].data_ptr(),
+                  self.world, self.rank, self._epoch, st["err"].data_ptr(), _lib.stream_ptr())
+
+    def check_errors(self) -> None:
+        """Raise if a peer barrier timed out (call after synchronising)."""
+        if self._p2p is not None and int(self._p2p["err"].item()):
+            raise RuntimeError("expert-parallel peer barrier timed out")
+
+    def _forward_p2p(self, x: torch.Tensor, out: torch.Tensor | None, timer):
+        if x.device != self.dev:
+            x = x.to(self.dev, non_blocking=True)
+        x = x.to(self.dtype).contiguous()
+        if x.dim() != 2 or x.shape[1] != self.M:
+            raise ShapeError(f"batch width {tuple(x.shape)} does not match layer hidden {self.M}")
+        S = x.shape[0]
+        ws = self._workspace(S)
+        st = self._p2p_state(S)
+        E, M, F, k, cap = self.E, self.M, self.F, self.k, st["cap"]
+        stream = _lib.stream_ptr()
+        ph = _Phases(timer)
+        ids, gp, lr, tc = ws["ids"], ws["gp"], ws["local_rank"], ws["tile_counts"]
+        out = torch.empty_like(x) if out is None else out
+        ph("gate")
+        if S:
+            _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k, None,
+                      ids.data_ptr(), gp.data_ptr(), lr.data_ptr(), tc.data_ptr(), stream)
+        _lib.call("moe_plan_scan", tc.data_ptr(), S, E, 2 ** 62, None,
+                  ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
+                  stream)
+        ph("counts_allgather")
+        # also orders this step after every rank's previous step (buffer reuse)
+        dist.all_gather_into_tensor(ws["counts"], ws["totals"], group=self.group)
+        ph("plan")
+        _lib.call("moe_ep_plan", ws["counts"].data_ptr(), self.world, self.rank, E, cap,
+                  st["slot_base"].data_ptr(), st["row_base"].data_ptr(),
+                  st["seg_start"].data_ptr(), st["seg_rows"].data_ptr(),
+                  st["recv_rows"].data_ptr(), stream)
+        _lib.call("moe_plan_scan", tc.data_ptr(), S, E, cap, st["slot_base"].data_ptr(),
+                  ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
+                  stream)
+        ph("dispatch_p2p")
+        if S:
+            _lib.call("moe_dispatch_p2p", x.data_ptr(), S, M * 2, E, k, cap, ids.data_ptr(),
+                      lr.data_ptr(), ws["tile_offsets"].data_ptr(), gp.data_ptr(),
+                      st["slot_base"].data_ptr(), st["row_base"].data_ptr(), self.E_loc,
+                      st["peer_recv"].data_ptr(), st["peer_tok"].data_ptr(),
+                      st["peer_prob"].data_ptr(), ws["slots"].data_ptr(),
+                      ws["row_index"].data_ptr(), out.data_ptr(), stream)
+        self._barrier(st)
+        G = self.E_loc
+        if cap:
+            ph("gemm1")
+            _lib.call("moe_grouped_gemm_bf16", st["recv"].data_ptr(), st["rmax"], M,
+                      self.w1.data_ptr(), self.E_loc * F, F, self.b1.data_ptr(),
+                      st["h"].data_ptr(), G, st["seg_start"].data_ptr(), 0,
+                      st["seg_rows"].data_ptr(), 0, st["seg_w"].data_ptr(), cap,
+                      _lib.MOE_ACT_GELU, stream)
+            ph("gemm2")  # + combine + residual, stored in the receive layout
+            _lib.call("moe_grouped_gemm_bf16_combine_rows", st["h"].data_ptr(), st["rmax"], F,
+                      self.w2.data_ptr(), self.E_loc * M, M, self.b2.data_ptr(), G,
+                      st["seg_start"].data_ptr(), st["seg_rows"].data_ptr(),
+                      st["seg_w"].data_ptr(), cap, st["row_token"].data_ptr(),
+                      st["row_prob"].data_ptr(), st["recv"].data_ptr(), st["ret"].data_ptr(),
+                      stream)
+        self._barrier(st)
+        ph("pull_p2p")
+        if S:
+            _lib.call("moe_pull_rows_p2p", S, M * 2, E, k, ids.data_ptr(),
+                      ws["row_index"].data_ptr(), self.E_loc, st["peer_ret"].data_ptr(),
+                      out.data_ptr(), stream)
+        ph(None)
+        return out
+
     def plan(self, S: int):
+        """(ids, gate_probs, global slots, plan) of the last forward; for the p2p
+        transport the plan is summarised as (cap, expert_load) from device tables."""
         ws = self._ws[S]
+        if self.transport == "p2p":
+            from types import SimpleNamespace
+
+            st = self._p2p
+            load = st["seg_rows"].cpu().numpy()
+            return ws["ids"], ws["gp"], ws["slots"], SimpleNamespace(cap=st["cap"],
+                                                                     expert_load=load)
         return ws["ids"], ws["gp"], ws["slots"], self.last_plan

@@ -58,12 +58,14 @@ class HostPipeline:
         cur.wait_event(self.ev_in[j])
         if self.started[j]:
             cur.wait_event(self.ev_out[j])
-        self.fn(self.x_dev[j], out=self.y_dev[j], **kw)
+        # (a layer may return its own output buffer instead of y_dev[j], e.g. the
+        # EP peer-memory output slots, which alternate in step with this pipeline)
+        y = self.fn(self.x_dev[j], out=self.y_dev[j], **kw)
         self.ev_used[j].record(cur)
         # download
         self.d2h.wait_event(self.ev_used[j])
         with torch.cuda.stream(self.d2h):
-            out_host.copy_(self.y_dev[j], non_blocking=True)
+            out_host.copy_(y, non_blocking=True)
             self.ev_out[j].record(self.d2h)
         self.started[j] = True
         return out_host

@@ -20,7 +20,7 @@ from paper_2201_05596_b200.ep import EPMoeLayer  # noqa: E402
 from paper_2201_05596_b200.gating import GatingConfig  # noqa: E402
 
 
-def run_case(S_loc, M, E, k, cf, residual, skew, seed):
+def run_case(S_loc, M, E, k, cf, residual, skew, seed, transport="auto"):
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", torch.cuda.current_device())
     spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=residual,
@@ -40,13 +40,19 @@ def run_case(S_loc, M, E, k, cf, residual, skew, seed):
                          torch.zeros(1, M, device=dev))
     params = A.MoeLayerParams(gate_w=gw, experts=tuple(ex), shared=sh)
     x_all = torch.randn(S_loc * world, M, device=dev, generator=g).to(torch.bfloat16)
-    full = A.MoeLayer(spec, params, dtype=torch.bfloat16, device=dev)
+    # the p2p transport fuses combine into GEMM2 like the single-GPU k=1 path;
+    # the nccl transport uses the separate combine kernel
+    full = A.MoeLayer(spec, params, dtype=torch.bfloat16, device=dev,
+                      fuse_combine=(transport == "p2p"))
     want = full(x_all)
     ids_f, gp_f, slots_f, load_f, cap_f = full.plan(S_loc * world)
-    ep = EPMoeLayer.from_params(spec, params)
+    ep = EPMoeLayer.from_params(spec, params, transport=transport)
     lo, hi = rank * S_loc, (rank + 1) * S_loc
     got = ep(x_all[lo:hi].clone())
+    got = ep(x_all[lo:hi].clone())  # second call: buffer reuse / slot alternation
     torch.cuda.synchronize()
+    if hasattr(ep, "check_errors"):
+        ep.check_errors()
     ids_e, gp_e, slots_e, plan = ep.plan(S_loc)
     assert plan.cap == cap_f, (plan.cap, cap_f)
     assert torch.equal(ids_e, ids_f[lo:hi]), "ids differ"
@@ -69,11 +75,16 @@ def main():
         (3000, 512, 8 * world, 1, 1.0, True, 1.0, 2),
         (2048, 2048, 32, 1, 1.0, False, 0.0, 3),
         (700, 256, 4 * world, 2, 0.6, False, 2.0, 4),
+        (2500, 1024, 16, 1, 0.8, False, 1.0, 5),
     ]
     for c in cases:
-        dropped = run_case(*c)
-        if dist.get_rank() == 0:
-            print(f"ep ok world={world} case={c} dropped_on_rank0={dropped}", flush=True)
+        for transport in ("nccl", "p2p"):
+            if transport == "p2p" and (c[3] != 1 or c[5]):
+                continue
+            dropped = run_case(*c, transport=transport)
+            if dist.get_rank() == 0:
+                print(f"ep ok world={world} transport={transport} case={c} "
+                      f"dropped_on_rank0={dropped}", flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -24,4 +24,5 @@ def test_ep_matches_single_gpu():
            os.path.join(ROOT, "tests", "ep_gpu_check.py")]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-5000:]
-    assert res.stdout.count("ep ok") == 4
+    assert res.stdout.count("transport=nccl") == 5
+    assert res.stdout.count("transport=p2p") == 2
