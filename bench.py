@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--tokens", type=int, default=C3["S"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--decode-iters", type=int, default=50)
     return ap.parse_args()
 
 
@@ -234,6 +236,30 @@ def run_gpu(args):
         ms = float(tt.item())
     phases = timer.summary(args.steps)
     kept = int(layer.kept_assignments(S)) if hasattr(layer, "kept_assignments") else S * k
+    # ---- decode (BASELINE config 5): p50 latency of one layer forward for small
+    # global batches at the same layer shape (weights streamed from HBM)
+    decode = {}
+    if not args.no_decode:
+        for sd in (64, 128, 256, 512):
+            s_loc = sd // world
+            xd = torch.randn(s_loc, M, device=dev, generator=gen).to(torch.bfloat16)
+            for _ in range(3):
+                layer(xd)
+            lat = []
+            for _ in range(args.decode_iters):
+                if world > 1:
+                    dist.barrier()
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record()
+                layer(xd)
+                a1.record()
+                a1.synchronize()
+                lat.append(a0.elapsed_time(a1))
+            lt = torch.tensor(lat, device=dev)
+            if world > 1:
+                dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+            decode[str(sd)] = round(float(lt.median().item()), 4)
     # ---- e2e through the public API: pinned host x -> layer(x) -> pinned host out.
     # Each step uploads its 268 MB batch and downloads its 268 MB result; the
     # layer streams host batches (H2D / forward / D2H overlapped across steps).
@@ -296,6 +322,7 @@ def run_gpu(args):
                      "peak_kind": f"{src} sustained (burst {tf_burst})",
                      "frac_of_burst": achieved / tf_burst if achieved else None},
         "phases_ms": phases,
+        "decode_p50_ms": decode or None,
         "kept_assignments_per_gpu": kept_rank,
         "cpu_baseline": cpu,
         "e2e": {"value": S * world / (e2e_ms * 1e-3), "unit": UNIT,

@@ -263,7 +263,8 @@ class MoeLayer:
         ws = self._ws.get(S)
         if ws is not None:
             return ws
-        self._ws.clear()
+        if len(self._ws) >= 4:  # keep a few batch sizes (e.g. prefill + decode) resident
+            self._ws.pop(next(iter(self._ws)))
         dev, dt, E, M, F, k = self.device, self.dtype, self.E, self.M, self.F, self.k
         cap = self.spec.gating.capacity(S)
         T = (S + _lib.ROUTE_TILE - 1) // _lib.ROUTE_TILE

@@ -205,7 +205,8 @@ class EPMoeLayer:
         ws = self._ws.get(S)
         if ws is not None:
             return ws
-        self._ws.clear()
+        if len(self._ws) >= 6:
+            self._ws.pop(next(iter(self._ws)))
         dev, E, M, F, k = self.dev, self.E, self.M, self.F, self.k
         T = (S + _lib.ROUTE_TILE - 1) // _lib.ROUTE_TILE
         i32 = dict(dtype=torch.int32, device=dev)
@@ -337,11 +338,12 @@ class EPMoeLayer:
 
     # ------------------------------------------------------------------ p2p
     def _p2p_state(self, S: int) -> dict:
-        st = self._p2p
-        if st is not None and st["S"] == S:
-            return st
+        """Peer-memory layout for batch size S (cached per S; collective on first use)."""
+        if self._p2p is None:
+            self._p2p = {}
+        st = self._p2p.get(S)
         if st is not None:
-            st["region"].close()
+            return st
         # the peer-memory layout is sized from the global batch: all ranks equal S
         sizes = torch.tensor([S], dtype=torch.int64, device=self.dev)
         alls = torch.empty(self.world, dtype=torch.int64, device=self.dev)
@@ -383,7 +385,7 @@ class EPMoeLayer:
             err=torch.zeros(1, **i32),
         )
         dist.barrier(group=self.group)
-        self._p2p = st
+        self._p2p[S] = st
         return st
 
     def _barrier(self, st: dict) -> None:
@@ -393,8 +395,9 @@ class EPMoeLayer:
 
     def check_errors(self) -> None:
         """Raise if a peer barrier timed out (call after synchronising)."""
-        if self._p2p is not None and int(self._p2p["err"].item()):
-            raise RuntimeError("expert-parallel peer barrier timed out")
+        for st in (self._p2p or {}).values():
+            if int(st["err"].item()):
+                raise RuntimeError("expert-parallel peer barrier timed out")
 
     def _forward_p2p(self, x: torch.Tensor, out: torch.Tensor | None, timer):
         if x.device != self.dev:
@@ -468,7 +471,7 @@ class EPMoeLayer:
         if self.transport == "p2p":
             from types import SimpleNamespace
 
-            st = self._p2p
+            st = self._p2p[S]
             load = st["seg_rows"].cpu().numpy()
             return ws["ids"], ws["gp"], ws["slots"], SimpleNamespace(cap=st["cap"],
                                                                      expert_load=load)
