@@ -34,6 +34,17 @@ sys.path.insert(0, ROOT)
 METRIC = "MoE-layer fwd tokens/s @1.3B+MoE-128 shape"
 UNIT = "tokens/s"
 C3 = dict(S=65536, M=2048, E=128, k=1, cf=1.0)
+# BASELINE.json configs as bench workloads (c3 is the headline / default)
+WORKLOADS = {
+    "c3": dict(S=65536, M=2048, E=128, k=1, cf=1.0, residual=False,
+               desc="C3: 1.3B+MoE-128 MoE layer (d_model 2048, d_ff 8192, 128 experts, top-1, cf 1.0)"),
+    "c2": dict(S=16384, M=1024, E=16, k=2, cf=1.25, residual=False,
+               desc="C2: top-2, cf 1.25 with drops, 16 experts, d_model 1024, 16384 tokens"),
+    "c4-32": dict(S=16384, M=1024, E=32, k=1, cf=1.0, residual=True,
+                  desc="C4: 350M+PR-MoE-32/64 layer with 32 experts + Residual-MoE shared MLP"),
+    "c4-64": dict(S=16384, M=1024, E=64, k=1, cf=1.0, residual=True,
+                  desc="C4: 350M+PR-MoE-32/64 layer with 64 experts + Residual-MoE shared MLP"),
+}
 
 
 def parse():
@@ -42,7 +53,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--tokens", type=int, default=C3["S"])
+    ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (default: workload's)")
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--decode-iters", type=int, default=50)
@@ -160,13 +172,14 @@ def peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def make_layer(S, M, E, k, cf, dev, seed=0):
+def make_layer(S, M, E, k, cf, dev, seed=0, residual=False):
     import torch
 
     from paper_2201_05596_b200 import arch as A
     from paper_2201_05596_b200.gating import GatingConfig
 
-    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, k, cf))
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=residual,
+                       gating=GatingConfig(E, k, cf))
     gen = torch.Generator(device=dev).manual_seed(seed)
     F = 4 * M
     # random-init weights of the named architecture: N(0,1)*0.1, zero biases (arch.py:347-365)
@@ -174,8 +187,13 @@ def make_layer(S, M, E, k, cf, dev, seed=0):
     w1 = torch.randn(E, M, F, device=dev, generator=gen, dtype=torch.bfloat16) * 0.1
     w2 = torch.randn(E, F, M, device=dev, generator=gen, dtype=torch.bfloat16) * 0.1
     zb1, zb2 = torch.zeros(1, F, device=dev), torch.zeros(1, M, device=dev)
+    shared = None
+    if residual:
+        shared = A.FfnParams(torch.randn(M, F, device=dev, generator=gen, dtype=torch.bfloat16) * 0.1,
+                             zb1, torch.randn(F, M, device=dev, generator=gen,
+                                              dtype=torch.bfloat16) * 0.1, zb2)
     p = A.MoeLayerParams(gate_w=gw, experts=tuple(A.FfnParams(w1[e], zb1, w2[e], zb2)
-                                                   for e in range(E)))
+                                                   for e in range(E)), shared=shared)
     layer = A.MoeLayer(spec, p, dtype=torch.bfloat16, device=dev)
     del w1, w2, p
     torch.cuda.empty_cache()
@@ -195,14 +213,16 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    S, M, E, k, cf = args.tokens, C3["M"], C3["E"], C3["k"], C3["cf"]
+    wl = WORKLOADS[args.workload]
+    S = args.tokens or wl["S"]
+    M, E, k, cf, residual = wl["M"], wl["E"], wl["k"], wl["cf"], wl["residual"]
     F = 4 * M
     if world > 1:
         from paper_2201_05596_b200.ep import EPMoeLayer
 
-        layer = EPMoeLayer.synthetic(S, M, E, k, cf, dev, seed=0)
+        layer = EPMoeLayer.synthetic(S, M, E, k, cf, dev, seed=0, residual=residual)
     else:
-        layer = make_layer(S, M, E, k, cf, dev)
+        layer = make_layer(S, M, E, k, cf, dev, residual=residual)
     gen = torch.Generator(device=dev).manual_seed(1 + rank)
     x = torch.randn(S, M, device=dev, generator=gen).to(torch.bfloat16)
     # drop-free synthetic routing at C3 with unbiased logits is ~1.9% drops
@@ -294,29 +314,32 @@ def run_gpu(args):
         return
     hbm, tf_burst, tf_sus, src = peaks()
     # dominant kernel: the grouped expert GEMM (GEMM1 + GEMM2 launches)
-    gemm_ms = sum(v for kk, v in phases.items() if kk.startswith("gemm"))
+    gemm_ms = sum(v for kk, v in phases.items() if kk.startswith("gemm") or kk == "shared_mlp")
     kept_rank = kept_total / world
-    flops = 4.0 * kept_rank * M * F  # 2*A*M*F per GEMM launch, two launches
+    # 2*A*M*F per expert GEMM launch (two launches), + 4*S*M*F for the shared MLP
+    flops = 4.0 * kept_rank * M * F + (4.0 * S * M * F if residual else 0.0)
     achieved = flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("grouped_gemm_bytes_per_step")
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.workload == "c3":
         dt, _ = cpu_reference_step()
         cpu = {"value": CPU_SAMPLE["S"] / dt, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
                "kind": "port", "sample": cpu_desc()}
     value = S * world / (ms * 1e-3)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC if args.workload == "c3" else f"MoE-layer fwd tokens/s @{args.workload}",
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "C3: 1.3B+MoE-128 MoE layer (d_model 2048, d_ff 8192, 128 experts,"
-                               " top-1, cf 1.0)", "tokens_per_gpu": S, "global_batch": S * world,
+        "config": {"workload": wl["desc"], "tokens_per_gpu": S, "global_batch": S * world,
                    "parallelism": f"ep{world}" if world > 1 else "single", "l2": "inputs larger "
                    "than L2 (x 268 MB, expert weights 8.6 GB per layer)"},
-        "roofline": {"bound": "tensor", "kernel": "grouped expert GEMM (GEMM1+GEMM2)",
+        "roofline": {"bound": "tensor",
+                     "kernel": "grouped expert GEMM (GEMM1+GEMM2" +
+                               (" + shared-MLP GEMMs)" if residual else ")"),
                      "achieved": achieved, "peak": tf_sus, "unit": "TFLOP/s",
                      "frac": achieved / tf_sus if achieved else None, "traffic": traffic,
                      "peak_kind": f"{src} sustained (burst {tf_burst})",

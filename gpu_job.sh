@@ -1,2 +1,3 @@
-CUDA_VISIBLE_DEVICES=0 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err; cat gpurun_out/bench.json
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 30 --warmup 3 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; tail -3 gpurun_out/bench_n2.err; cat gpurun_out/bench_n2.json
+python tools/gemm_bench.py --env MOE_STORE_HINT --variants 0,1 --rounds 3
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-decode"
+for h in 0 1; do MOE_STORE_HINT=$h $CMD > gpurun_out/plain.log 2>&1 && MOE_STORE_HINT=$h ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"gemm_bf16" --csv --log-file gpurun_out/hint$h.csv $CMD > gpurun_out/ncu_launch.log 2>&1; done

@@ -69,6 +69,7 @@ struct GemmArgs {
   // row is stored at the same row of `out` (receive layout); the source rank then
   // pulls it over NVLink
   int x_by_row;
+  int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
 };
 
 // CG = 1: one CTA computes a BM x BN tile (tcgen05.mma.cta_group::1, M=128).
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
     uint32_t acc_phase = 0;
     int g = 0;
     const int N = args.N;
+    const uint64_t pol_stream = policy_evict_first();
     for (int tile = work_id; tile < total_tiles; tile += work_stride) {
       int mb, nb;
       decode(tile, g, mb, nb);
@@ -335,7 +337,8 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
             if (valid && vec_ok && col0 + 32 <= N) {
               const uint4* xs = reinterpret_cast<const uint4*>(xrow + col0);
 #pragma unroll
-              for (int q = 0; q < 4; ++q) xq[q] = __ldg(xs + q);
+              for (int q = 0; q < 4; ++q)
+                xq[q] = args.stream_hint ? ld_global_nc_hint(xs + q, pol_stream) : __ldg(xs + q);
             }
           }
           tmem_ld_wait_regs(r[c & 1]);
@@ -367,7 +370,10 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
               pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
               pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
               pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-              dst[q] = pk;
+              if (args.stream_hint)
+                st_global_hint(dst + q, pk, pol_stream);
+              else
+                dst[q] = pk;
             }
           } else {
 #pragma unroll
@@ -587,6 +593,10 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
     const char* v = getenv("MOE_GEMM_VARIANT");
     return v ? atoi(v) : 0;
   }();
+  static const int stream_hint = [] {
+    const char* v = getenv("MOE_STORE_HINT");
+    return v ? atoi(v) : 1;
+  }();
   const int CG = (BN == 256 && max_group_rows > BM && variant != 2) ? 2 : 1;
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, a_rows, K, BM);
@@ -609,6 +619,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.x_resid = (const __nv_bfloat16*)x_resid;
   a.out = (__nv_bfloat16*)out;
   a.x_by_row = x_by_row;
+  a.stream_hint = stream_hint;
   const int64_t nblk = (N + BN - 1) / BN;
   const int64_t tm = (int64_t)BM * CG;
   const int64_t max_tiles = (int64_t)G * ((max_group_rows + tm - 1) / tm) * nblk;

@@ -179,13 +179,15 @@ class EPMoeLayer:
         return cls(spec, params.gate_w, local, params.shared, group=group, **kw)
 
     @classmethod
-    def synthetic(cls, S: int, M: int, E: int, k: int, cf: float, dev, seed: int = 0, group=None):
+    def synthetic(cls, S: int, M: int, E: int, k: int, cf: float, dev, seed: int = 0, group=None,
+                  residual: bool = False):
         """Random-init layer of the named shape (N(0,1)*0.1 weights, zero biases,
         arch.py:347-365), generated on device per expert so every rank draws
         the same gate and its own expert block."""
         from .arch import FfnParams
 
-        spec = LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, k, cf))
+        spec = LayerSpec(kind="moe", hidden=M, experts=E, residual=residual,
+                         gating=GatingConfig(E, k, cf))
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         e_loc = E // world
         g = torch.Generator(device=dev).manual_seed(seed)
@@ -198,7 +200,13 @@ class EPMoeLayer:
             w1 = torch.randn(M, F, device=dev, generator=ge, dtype=torch.bfloat16) * 0.1
             w2 = torch.randn(F, M, device=dev, generator=ge, dtype=torch.bfloat16) * 0.1
             experts.append(FfnParams(w1, zb1, w2, zb2))
-        return cls(spec, gate_w, experts, None, group=group, device=dev)
+        shared = None
+        if residual:  # replicated: same draw on every rank
+            gs = torch.Generator(device=dev).manual_seed(seed * 100003 + E + 1)
+            shared = FfnParams(torch.randn(M, F, device=dev, generator=gs, dtype=torch.bfloat16) * 0.1,
+                               zb1, torch.randn(F, M, device=dev, generator=gs,
+                                                dtype=torch.bfloat16) * 0.1, zb2)
+        return cls(spec, gate_w, experts, shared, group=group, device=dev)
 
     # ------------------------------------------------------------------
     def _workspace(self, S: int) -> dict:

@@ -49,7 +49,7 @@ def child(iters: int) -> None:
         torch.cuda.synchronize()
         t1 += ev[0].elapsed_time(ev[1]); t2 += ev[1].elapsed_time(ev[2])
     fl = 2.0 * G * cap * M * F
-    print(json.dumps({"variant": os.environ.get("MOE_GEMM_VARIANT", "0"),
+    print(json.dumps({"variant": {k: v for k, v in os.environ.items() if k.startswith("MOE_")},
                       "gemm1_ms": t1 / iters, "gemm2_ms": t2 / iters,
                       "gemm1_tflops": fl / (t1 / iters) / 1e9, "gemm2_tflops": fl / (t2 / iters) / 1e9}))
 
@@ -60,13 +60,14 @@ def main():
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--env", default="MOE_GEMM_VARIANT", help="env var the variants set")
     a = ap.parse_args()
     if a.child:
         child(a.iters)
         return
     for _ in range(a.rounds):
         for v in a.variants.split(","):
-            env = dict(os.environ, MOE_GEMM_VARIANT=v)
+            env = dict(os.environ, **{a.env: v})
             out = subprocess.run([sys.executable, __file__, "--child", "--iters", str(a.iters)],
                                  env=env, capture_output=True, text=True)
             print(out.stdout.strip() or out.stderr[-2000:], flush=True)
