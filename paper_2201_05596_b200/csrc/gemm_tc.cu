@@ -70,6 +70,7 @@ struct GemmArgs {
   // pulls it over NVLink
   int x_by_row;
   int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
+  int raster;       // tile order (see tile_at)
 };
 
 // CG = 1: one CTA computes a BM x BN tile (tcgen05.mma.cta_group::1, M=128).
@@ -171,15 +172,30 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = tile_start[G];
 
-  // tile -> (group, m block, n block); n-major within a group so CTAs that run
-  // concurrently share the B (weight) tile through L2.
+  // Work order: tiles are numbered (group, m block, n block) with n fastest and
+  // each cluster takes runs of kRun consecutive tiles: kRun n-blocks of the same
+  // activation rows, so the A tile its own SMs just streamed is re-read from L2
+  // a tile later (temporal locality inside the cluster), while the clusters that
+  // run the other m-blocks of the same n-blocks share each weight tile.
+  // args.raster: 0 = plain round robin with m fastest (concurrent clusters share
+  // the weight tile), 1 = round robin over runs of 4 n-blocks with n fastest.
+  const int kRun = args.raster == 1 ? 4 : 1;
+  auto tile_at = [&](int it) {
+    return ((it / kRun) * work_stride + work_id) * kRun + (it % kRun);
+  };
+  // tile -> (group, m block, n block)
   auto decode = [&](int tile, int& g, int& mb, int& nb) {
     while (tile_start[g + 1] <= tile) ++g;
     const int local = tile - tile_start[g];
     const int64_t r = args.rows ? args.rows[g] : args.rows_const;
-    const int mblocks = (int)((r + TM - 1) / TM);
-    nb = local / mblocks;
-    mb = local - nb * mblocks;
+    if (args.raster == 1) {
+      mb = local / n_blocks;
+      nb = local - mb * n_blocks;
+    } else {
+      const int mblocks = (int)((r + TM - 1) / TM);
+      nb = local / mblocks;
+      mb = local - nb * mblocks;
+    }
   };
 
   if (warp == 0) {
@@ -190,7 +206,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
     const int num_kb = (args.K + BK - 1) / BK;
     // (L2 eviction-priority hints on A/B were measured and removed: evict_first
     // on the weights raised DRAM traffic from 6.2 to 9.1 GB per GEMM1 launch)
-    for (int tile = work_id; tile < total_tiles; tile += work_stride) {
+    for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int mb, nb;
       decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
@@ -230,7 +246,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const int num_kb = (args.K + BK - 1) / BK;
-    for (int tile = work_id; leader && tile < total_tiles; tile += work_stride) {
+    for (int it = 0, tile = tile_at(0); leader && tile < total_tiles; tile = tile_at(++it)) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -285,7 +301,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
     int g = 0;
     const int N = args.N;
     const uint64_t pol_stream = policy_evict_first();
-    for (int tile = work_id; tile < total_tiles; tile += work_stride) {
+    for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int mb, nb;
       decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
@@ -597,6 +613,10 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
     const char* v = getenv("MOE_STORE_HINT");
     return v ? atoi(v) : 1;
   }();
+  static const int raster = [] {
+    const char* v = getenv("MOE_RASTER");
+    return v ? atoi(v) : 0;
+  }();
   const int CG = (BN == 256 && max_group_rows > BM && variant != 2) ? 2 : 1;
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, a_rows, K, BM);
@@ -620,6 +640,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.out = (__nv_bfloat16*)out;
   a.x_by_row = x_by_row;
   a.stream_hint = stream_hint;
+  a.raster = raster;
   const int64_t nblk = (N + BN - 1) / BN;
   const int64_t tm = (int64_t)BM * CG;
   const int64_t max_tiles = (int64_t)G * ((max_group_rows + tm - 1) / tm) * nblk;
