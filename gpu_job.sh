@@ -1,1 +1,1 @@
-python tools/gemm_bench.py --env MOE_RASTER --variants 0,1 --rounds 4
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -15

@@ -132,6 +132,24 @@ int moe_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E,
                        float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,
                        int32_t* tile_counts, void* stream);
 
+/* As moe_gate_gemm_bf16, plus probsum (E) f32 += column sums of the full
+ * softmax over the batch (caller zero-fills): with the plan scan's pre-drop
+ * totals this gives the load-balance loss without re-reading anything. */
+int moe_gate_gemm_bf16_stats(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
+                             float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,
+                             int32_t* tile_counts, float* probsum, void* stream);
+
+/* arch.load_balance_loss (arch.py:297-313): E * sum_e f_e * P_e with pre-drop
+ * assignment fractions f_e = count_e / (S k) and P_e = mean_t probs[t, e],
+ * written as one float64 to *out. From ids (S, k) + probs (S, E) f32|f64 with
+ * a 2E-double workspace, or from the fused gate's statistics (counts = the
+ * plan scan's totals, probsum from moe_gate_gemm_bf16_stats). */
+size_t moe_load_balance_workspace_bytes(int E);
+int moe_load_balance_loss(const int32_t* ids, int64_t S, int E, int k, const void* probs, int dtype,
+                          double* out, void* ws, size_t ws_bytes, void* stream);
+int moe_load_balance_loss_from_stats(const int32_t* counts, const float* probsum, int64_t S, int E,
+                                     int k, double* out, void* stream);
+
 /* Grouped expert GEMM on tcgen05 (the two halves of forward_ffn,
  * arch.py:368-369): for each group g with rows[g] rows starting at row
  * row_start[g] (or g*row_stride when row_start is NULL) of A (a_rows, K):

@@ -4,7 +4,7 @@ gating / layer API (arXiv 2201.05596). See DESIGN.md and INTEGRATION.md."""
 from . import arch, gating, tensor  # noqa: F401
 from .arch import (  # noqa: F401
     FFN_MULT, FfnParams, LayerSpec, MoeLayer, MoeLayerParams, ValidationError, forward_ffn,
-    forward_layer, init_layer_params,
+    forward_layer, init_layer_params, load_balance_loss,
 )
 from .gating import (  # noqa: F401
     DROPPED, DispatchPlan, ExpertBuffers, GatingConfig, OpCounter, TopKGate, build_dispatch_plan,

@@ -44,6 +44,10 @@ SIGNATURES = {
     "moe_dispatch_fused": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "moe_combine": (_I, [_P, _I, _L, _I, _I, _I, _L, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P]),
     "moe_gate_gemm_bf16": (_I, [_P, _P, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "moe_gate_gemm_bf16_stats": (_I, [_P, _P, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "moe_load_balance_workspace_bytes": (_Z, [_I]),
+    "moe_load_balance_loss": (_I, [_P, _L, _I, _I, _P, _I, _P, _P, _Z, _P]),
+    "moe_load_balance_loss_from_stats": (_I, [_P, _P, _L, _I, _I, _P, _P]),
     "moe_grouped_gemm_bf16": (_I, [_P, _L, _I, _P, _L, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L,
                                    _I, _P]),
     "moe_grouped_gemm_bf16_combine": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _L, _P, _L, _P,
@@ -140,6 +144,7 @@ def dtype_code(dt: torch.dtype) -> int:
 # ---------------------------------------------------------------------------
 
 _NON_LAUNCH = {"moe_abi_version", "moe_plan_workspace_bytes", "moe_scan_workspace_bytes",
+               "moe_load_balance_workspace_bytes",
                "moe_ipc_malloc", "moe_ipc_free", "moe_ipc_get_handle", "moe_ipc_open_handle",
                "moe_ipc_close_handle"}
 # entry points that launch more than one kernel per call

@@ -41,6 +41,7 @@ __all__ = [
     "forward_layer",
     "MoeLayer",
     "DenseFfn",
+    "load_balance_loss",
 ]
 
 FFN_MULT = 4  # arch.py:65
@@ -213,7 +214,7 @@ class MoeLayer:
     """
 
     def __init__(self, spec: LayerSpec, params: MoeLayerParams, dtype=torch.bfloat16,
-                 device=None, fuse_combine: bool = True) -> None:
+                 device=None, fuse_combine: bool = True, aux_loss: bool = False) -> None:
         if spec.kind != "moe":
             raise ValidationError("MoeLayer needs a moe LayerSpec")
         dev = _lib.require_device(None) if device is None else torch.device(device)
@@ -257,6 +258,7 @@ class MoeLayer:
                                   self.k == 1 and self.shared is None)
         self._ws: dict = {}
         self._pipe = None
+        self.aux_loss = aux_loss
 
     # -- workspace -----------------------------------------------------------
     def workspace(self, S: int) -> dict:
@@ -283,6 +285,8 @@ class MoeLayer:
         )
         if dt == torch.float32:
             ws["logits"] = torch.empty((S, E), dtype=torch.float32, device=dev)
+        ws["probsum"] = torch.zeros(E, dtype=torch.float32, device=dev)
+        ws["aux"] = torch.zeros(1, dtype=torch.float64, device=dev)
         if self.fused_combine:
             ws["row_token"] = torch.empty(max(E * cap, 1), **i32)
             ws["row_prob"] = torch.empty(max(E * cap, 1), dtype=torch.float32, device=dev)
@@ -296,6 +300,11 @@ class MoeLayer:
     def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None,
                  logits_out: torch.Tensor | None = None, timer=None) -> torch.Tensor:
         return self.forward(x, out, logits_out, timer)
+
+    # load-balance loss of the last forward (arch.py:297-313), when aux_loss=True:
+    # the fused gate accumulates the softmax column sums, the plan scan the counts
+    aux_loss: bool = False
+    last_aux_loss: torch.Tensor | None = None
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None,
                 logits_out: torch.Tensor | None = None, timer=None) -> torch.Tensor:
@@ -335,20 +344,43 @@ class MoeLayer:
         ids, gp, lr, tc = ws["ids"], ws["gp"], ws["local_rank"], ws["tile_counts"]
         ph = _Phases(timer)
         ph("gate")
+        aux = self.aux_loss
         if self.dtype == torch.bfloat16:
-            _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k,
-                      _lib.ptr(logits_out), ids.data_ptr(), gp.data_ptr(), lr.data_ptr(),
-                      tc.data_ptr(), st)
+            if aux:
+                ws["probsum"].zero_()
+                _lib.call("moe_gate_gemm_bf16_stats", x.data_ptr(), self.wg.data_ptr(), S, M, E,
+                          k, _lib.ptr(logits_out), ids.data_ptr(), gp.data_ptr(), lr.data_ptr(),
+                          tc.data_ptr(), ws["probsum"].data_ptr(), st)
+            else:
+                _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k,
+                          _lib.ptr(logits_out), ids.data_ptr(), gp.data_ptr(), lr.data_ptr(),
+                          tc.data_ptr(), st)
         else:
             logits = ws["logits"] if logits_out is None else logits_out
             _grouped_gemm(self.dtype, x, S, M, self.wg, E, None, logits, 1, None, 0, None, S, S,
                           _lib.MOE_ACT_NONE)
+            probs = None
+            if aux:
+                probs = ws.setdefault("probs", torch.empty((S, E), dtype=torch.float32,
+                                                           device=self.device))
             _lib.call("moe_topk_gate", logits.data_ptr(), _lib.MOE_F32, S, E, k, ids.data_ptr(),
-                      gp.data_ptr(), None, st)
+                      gp.data_ptr(), _lib.ptr(probs), st)
             _lib.call("moe_plan_tiles", ids.data_ptr(), S, E, k, lr.data_ptr(), tc.data_ptr(), st)
         ph("scan")
         _lib.call("moe_plan_scan", tc.data_ptr(), S, E, cap, None, ws["tile_offsets"].data_ptr(),
                   ws["totals"].data_ptr(), ws["load"].data_ptr(), st)
+        if aux:
+            if self.dtype == torch.bfloat16:
+                _lib.call("moe_load_balance_loss_from_stats", ws["totals"].data_ptr(),
+                          ws["probsum"].data_ptr(), S, E, k, ws["aux"].data_ptr(), st)
+            else:
+                lib = _lib.load()
+                wsb = lib.moe_load_balance_workspace_bytes(E)
+                scratch = ws.setdefault("aux_ws", torch.empty(wsb // 8, dtype=torch.float64,
+                                                              device=self.device))
+                _lib.call("moe_load_balance_loss", ids.data_ptr(), S, E, k, ws["probs"].data_ptr(),
+                          _lib.MOE_F32, ws["aux"].data_ptr(), scratch.data_ptr(), wsb, st)
+            self.last_aux_loss = ws["aux"]
         ph("dispatch")
         if self.fused_combine:
             _lib.call("moe_dispatch_fused", x.data_ptr(), S, M * x.element_size(), E, k, cap,
@@ -400,6 +432,32 @@ class MoeLayer:
 # ---------------------------------------------------------------------------
 # reference-shaped entry points
 # ---------------------------------------------------------------------------
+
+
+def load_balance_loss(plan, probs) -> float:
+    """E * sum_e (assignment fraction_e) * (mean gate prob_e), fractions taken
+    before capacity drops (arch.py:297-313), computed on the device in float64."""
+    from .gating import _dev, _is_torch
+
+    as_np = not _is_torch(probs)
+    p = np.asarray(probs, dtype=np.float64) if as_np else probs
+    e = plan.num_experts
+    if len(p.shape) != 2 or tuple(p.shape) != (plan.num_tokens, e):
+        raise ShapeError(f"probs shape {tuple(p.shape)} does not match plan")
+    if plan.num_tokens == 0:
+        return 0.0
+    pd = _dev(p)
+    if pd.dtype not in (torch.float32, torch.float64):
+        pd = pd.float()
+    ids = _dev(np.asarray(plan.expert_ids, dtype=np.int32) if not _is_torch(plan.expert_ids)
+               else plan.expert_ids, torch.int32).to(pd.device)
+    lib = _lib.load()
+    wsb = lib.moe_load_balance_workspace_bytes(e)
+    ws = torch.empty(wsb // 8, dtype=torch.float64, device=pd.device)
+    out = torch.empty(1, dtype=torch.float64, device=pd.device)
+    _lib.call("moe_load_balance_loss", ids.data_ptr(), plan.num_tokens, e, plan.k, pd.data_ptr(),
+              _lib.dtype_code(pd.dtype), out.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr())
+    return float(out.item())
 
 
 def _input(x):

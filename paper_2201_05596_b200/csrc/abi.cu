@@ -180,6 +180,35 @@ int moe_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E,
                                     tile_counts, S_(stream));
 }
 
+int moe_gate_gemm_bf16_stats(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
+                             float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,
+                             int32_t* tile_counts, float* probsum, void* stream) {
+  CHECK(S >= 0 && M >= 8 && M % 8 == 0 && E >= 1 && E <= 256 && (k == 1 || k == 2) && k <= E);
+  if (S == 0) return MOE_OK;
+  CHECK(x && wg_t && ids && gate_probs && local_rank && tile_counts && probsum);
+  return moe::launch_gate_gemm_bf16(x, wg_t, S, M, E, k, logits, ids, gate_probs, local_rank,
+                                    tile_counts, S_(stream), probsum);
+}
+
+size_t moe_load_balance_workspace_bytes(int E) { return E < 1 ? 0 : 2 * (size_t)E * sizeof(double); }
+
+int moe_load_balance_loss(const int32_t* ids, int64_t S, int E, int k, const void* probs, int dtype,
+                          double* out, void* ws, size_t ws_bytes, void* stream) {
+  CHECK(S >= 0 && E >= 1 && (k == 1 || k == 2) && out && ws);
+  CHECK(ws_bytes >= moe_load_balance_workspace_bytes(E));
+  CHECK(dtype == MOE_F32 || dtype == MOE_F64);
+  if (S > 0) CHECK(ids && probs);
+  return moe::launch_aux_loss(ids, S, k, E, probs, dtype, nullptr, nullptr, out,
+                              static_cast<double*>(ws), S_(stream));
+}
+
+int moe_load_balance_loss_from_stats(const int32_t* counts, const float* probsum, int64_t S, int E,
+                                     int k, double* out, void* stream) {
+  CHECK(S >= 0 && E >= 1 && (k == 1 || k == 2) && counts && probsum && out);
+  return moe::launch_aux_loss(nullptr, S, k, E, nullptr, MOE_F32, counts, probsum, out, nullptr,
+                              S_(stream));
+}
+
 int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
                           int N, const float* bias, void* D, int num_groups,
                           const int32_t* row_start, int64_t row_stride, const int32_t* rows,

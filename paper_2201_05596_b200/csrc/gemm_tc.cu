@@ -60,6 +60,7 @@ struct GemmArgs {
   float* gate_probs;          // [S, k]
   int32_t* local_rank;        // [S, k]
   int32_t* tile_counts;       // [T, E]
+  float* probsum;             // [E] optional: column sums of the softmax (load-balance loss)
   // fused combine epilogue
   const int32_t* row_token;   // [a_rows] token of each expert-buffer row
   const float* row_prob;      // [a_rows] its gate probability
@@ -301,6 +302,13 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
     int g = 0;
     const int N = args.N;
     const uint64_t pol_stream = policy_evict_first();
+    if constexpr (EPI == EPI_GATE) {
+      if (args.probsum != nullptr) {
+        float* psum = reinterpret_cast<float*>(smem + L::kTileOff) + 8 + 4 * args.E;
+        for (int i = (warp - 2) * 32 + lane; i < args.E; i += 128) psum[i] = 0.f;
+        named_bar_sync(1, 128);
+      }
+    }
     for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int mb, nb;
       decode(tile, g, mb, nb);
@@ -447,6 +455,33 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
           for (int i = 0; i < 32; ++i)
             if (c * 32 + i < E) sum += expf(__uint_as_float(r[i]) - b1);
         }
+        if (args.probsum != nullptr) {
+          // load-balance statistics (arch.py:297-313): column sums of the full softmax,
+          // reduced across the warp with a transpose-reduce (lane l ends with column l)
+          const float inv = 1.f / sum;
+          float* psum = reinterpret_cast<float*>(smem + L::kTileOff) + 8 + 4 * E;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(t_addr + c * 32, r);
+            tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              v[i] = (valid && c * 32 + i < E) ? expf(__uint_as_float(r[i]) - b1) * inv : 0.f;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+              const bool upper = (lane & off) != 0;
+#pragma unroll
+              for (int i = 0; i < off; ++i) {
+                const float send = upper ? v[i] : v[i + off];
+                const float keep = upper ? v[i + off] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+              }
+            }
+            if (c * 32 + (int)lane < E) atomicAdd(&psum[c * 32 + lane], v[0]);
+          }
+        }
         // accumulator consumed: hand TMEM back to the MMA warp
         tc_fence_before();
         __syncwarp();
@@ -503,6 +538,13 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
+      }
+    }
+    if constexpr (EPI == EPI_GATE) {
+      if (args.probsum != nullptr) {  // one global atomic per expert per CTA
+        named_bar_sync(1, 128);
+        const float* psum = reinterpret_cast<const float*>(smem + L::kTileOff) + 8 + 4 * args.E;
+        for (int i = (warp - 2) * 32 + lane; i < args.E; i += 128) atomicAdd(&args.probsum[i], psum[i]);
       }
     }
   }
@@ -677,7 +719,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
 
 int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
                           float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,
-                          int32_t* tile_counts, cudaStream_t st) {
+                          int32_t* tile_counts, cudaStream_t st, float* probsum) {
   if (S == 0) return 0;
   if (E < 1 || E > 256 || (M % 8) != 0 || k < 1 || k > 2) return MOE_EINVAL;
   int BN = 32;
@@ -701,6 +743,7 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   a.gate_probs = gate_probs;
   a.local_rank = local_rank;
   a.tile_counts = tile_counts;
+  a.probsum = probsum;
   const int64_t tiles = (S + BM - 1) / BM;
   switch (BN) {
     case 32: return launch_tc<32, 8, EPI_GATE>(ma, mb, a, tiles, st);

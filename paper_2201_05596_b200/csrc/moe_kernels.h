@@ -73,7 +73,12 @@ int launch_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int r
 
 int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
                           float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,
-                          int32_t* tile_counts, cudaStream_t st);
+                          int32_t* tile_counts, cudaStream_t st, float* probsum = nullptr);
+
+// load-balance loss (arch.py:297-313)
+int launch_aux_loss(const int32_t* ids, int64_t S, int k, int E, const void* probs, int dtype,
+                    const int32_t* counts, const float* probsum, double* out, double* ws,
+                    cudaStream_t st);
 
 int launch_grouped_gemm_f32(const float* A, int K, const float* B, int N, const float* bias,
                             float* D, int G, const int32_t* row_start, int64_t row_stride,

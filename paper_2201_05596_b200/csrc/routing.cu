@@ -455,6 +455,62 @@ __global__ void combine_kernel(const T* __restrict__ y, int64_t S, int M, int k,
   }
 }
 
+// ============================================================ load-balance loss
+// E * sum_e (count_e / (S k)) * (mean_t probs[t, e]) with pre-drop counts
+// (arch.py:297-313). Statistics in float64.
+template <typename T>
+__global__ void aux_stats_kernel(const int32_t* __restrict__ ids, int64_t S, int k, int E,
+                                 const T* __restrict__ probs, double* __restrict__ ws) {
+  const int64_t rows_per = (S + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(S, r0 + rows_per);
+  for (int c = threadIdx.x; c < E; c += blockDim.x) {
+    double acc = 0.0;
+    for (int64_t r = r0; r < r1; ++r) acc += (double)probs[r * E + c];
+    if (r1 > r0) atomicAdd(&ws[c], acc);
+  }
+  for (int64_t a = r0 * k + threadIdx.x; a < r1 * k; a += blockDim.x)
+    atomicAdd(&ws[E + ids[a]], 1.0);
+}
+
+__global__ void aux_finalize_kernel(int64_t S, int k, int E, const double* __restrict__ ws,
+                                    const int32_t* __restrict__ counts,
+                                    const float* __restrict__ probsum, double* out) {
+  __shared__ double part[32];
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const double cnt = counts ? (double)counts[e] : ws[E + e];
+    const double ps = probsum ? (double)probsum[e] : ws[e];
+    acc += (cnt / ((double)S * k)) * (ps / (double)S);
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+    out[0] = S > 0 ? (double)E * t : 0.0;
+  }
+}
+
+int launch_aux_loss(const int32_t* ids, int64_t S, int k, int E, const void* probs, int dtype,
+                    const int32_t* counts, const float* probsum, double* out, double* ws,
+                    cudaStream_t st) {
+  if (counts == nullptr || probsum == nullptr) {
+    cudaMemsetAsync(ws, 0, 2 * (size_t)E * sizeof(double), st);
+    if (S > 0) {
+      const int g = (int)(S < 148 * 4 ? S : 148 * 4);
+      if (dtype == MOE_F64)
+        aux_stats_kernel<double><<<g, 256, 0, st>>>(ids, S, k, E, (const double*)probs, ws);
+      else if (dtype == MOE_F32)
+        aux_stats_kernel<float><<<g, 256, 0, st>>>(ids, S, k, E, (const float*)probs, ws);
+      else
+        return MOE_EINVAL;
+    }
+  }
+  aux_finalize_kernel<<<1, 256, 0, st>>>(S, k, E, ws, counts, probsum, out);
+  return (int)cudaGetLastError();
+}
+
 // ============================================================ launchers
 static int grid_for(int64_t work, int per_block, int cap_blocks = 148 * 32) {
   int64_t g = (work + per_block - 1) / per_block;

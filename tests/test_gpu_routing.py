@@ -179,3 +179,79 @@ def test_device_tensors_stay_on_device():
     kept = (plan.slots >= 0).float()
     w = (gate.gate_probs * kept).sum(1, keepdim=True)
     torch.testing.assert_close(out.float(), x.float() * w, rtol=1e-2, atol=1e-2)
+
+
+def test_ep_plan_kernel_matches_host_plan():
+    """moe_ep_plan (device exchange plan of the peer-memory EP transport) against a
+    NumPy restatement, for simulated worlds of 2/4/8 ranks (pure function of the
+    all-gathered counts, so one GPU covers every rank's view)."""
+    from paper_2201_05596_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    for world in (1, 2, 4, 8):
+        E = 16 * world
+        counts = rng.integers(0, 700, size=(world, E)).astype(np.int32)
+        cap = int(counts.sum(0).mean())
+        e_loc = E // world
+        base = np.zeros_like(counts, dtype=np.int64)
+        base[1:] = np.cumsum(counts, 0)[:-1]
+        kept = np.clip(cap - base, 0, counts)
+        for rank in range(world):
+            c_d = torch.from_numpy(counts).cuda().reshape(-1)
+            out = [torch.empty(E, dtype=torch.int32, device="cuda") for _ in range(2)]
+            seg = [torch.empty(e_loc, dtype=torch.int32, device="cuda") for _ in range(2)]
+            rr = torch.empty(1, dtype=torch.int32, device="cuda")
+            _lib.call("moe_ep_plan", c_d.data_ptr(), world, rank, E, cap, out[0].data_ptr(),
+                      out[1].data_ptr(), seg[0].data_ptr(), seg[1].data_ptr(), rr.data_ptr(),
+                      _lib.stream_ptr())
+            assert np.array_equal(out[0].cpu().numpy(), base[rank])
+            # expert-major receive layout on each owner: [local expert][source][slot]
+            row_base = np.zeros(E, dtype=np.int64)
+            for e in range(E):
+                o, el = divmod(e, e_loc)
+                blk = kept[:, o * e_loc:o * e_loc + el].sum()
+                row_base[e] = blk + kept[:rank, e].sum()
+            assert np.array_equal(out[1].cpu().numpy(), row_base)
+            mine = kept[:, rank * e_loc:(rank + 1) * e_loc].sum(0)
+            assert np.array_equal(seg[1].cpu().numpy(), mine)
+            assert np.array_equal(seg[0].cpu().numpy(), np.concatenate([[0], np.cumsum(mine)[:-1]]))
+            assert int(rr.item()) == int(mine.sum())
+
+
+def test_load_balance_loss_golden_and_api():
+    """arch.load_balance_loss on the device against the reference's values
+    (tests/golden/plans.npz, generated with moekit.arch.load_balance_loss)."""
+    from paper_2201_05596_b200 import arch as A
+
+    z = _load("plans.npz")
+    for i in range(int(z["n"])):
+        e, k, cf = z[f"p{i}_cfg"]
+        cfg = G.GatingConfig(int(e), int(k), float(cf))
+        lg = z[f"p{i}_logits"]
+        gate = G.top_k_gate(lg, cfg)
+        plan = G.build_dispatch_plan(gate, cfg, lg.shape[0])
+        got = A.load_balance_loss(plan, gate.probs)
+        assert abs(got - float(z[f"p{i}_lbl"])) <= 1e-12 * max(1.0, abs(got)), i
+    with pytest.raises(ValueError):
+        A.load_balance_loss(plan, np.zeros((3, 3)))
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_fused_aux_loss_matches_oracle(dtype):
+    """The gate epilogue's softmax column sums + the scan's pre-drop counts give
+    the same load-balance loss as the oracle on the layer's own logits."""
+    from paper_2201_05596_b200 import arch as A
+
+    S, M, E, k = 3000, 256, 16, 2
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=G.GatingConfig(E, k, 1.0))
+    p = A.init_layer_params(spec, np.random.default_rng(4))
+    p.gate_w.value[:] += np.random.default_rng(5).normal(0, 0.3, (1, E))
+    layer = A.MoeLayer(spec, p, dtype=dtype)
+    layer.aux_loss = True
+    x = torch.randn(S, M, device="cuda").to(dtype)
+    logits = torch.empty(S, E, device="cuda")
+    layer(x, logits_out=logits)
+    got = float(layer.last_aux_loss.item())
+    ids, _, probs = O.top_k_gate(logits.double().cpu().numpy(), E, k)
+    want = O.load_balance_loss(ids, probs, E, k)
+    assert abs(got - want) <= 1e-5 * want
