@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -15
+timeout 600 python -m pytest tests/test_gpu_route_bench.py -x -q -p no:cacheprovider 2>&1 | tail -5

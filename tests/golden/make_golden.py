@@ -208,7 +208,26 @@ def layers():
     _save("layers.npz", **out)
 
 
+def route_bench():
+    # the reference CLI's route-bench verb (cli.py:260-306) on two configs
+    import json
+    import tempfile
+
+    from moekit.cli import main
+
+    for name, opts, seed in [("route_bench_a.csv", {"tokens": 300, "experts": 8, "k": 2,
+                                                     "capacity_factor": 1.0, "instances": 5}, 7),
+                             ("route_bench_b.csv", {"tokens": 1000, "experts": 16, "k": 1,
+                                                     "capacity_factor": 0.5, "instances": 3}, 11)]:
+        with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+            json.dump({"seed": seed, "options": opts}, f)
+        rc = main(["route-bench", "--config", f.name, "--out", os.path.join(HERE, name)])
+        assert rc == 0
+        print("wrote", name)
+
+
 if __name__ == "__main__":
+    route_bench()
     gate_kats()
     scans()
     plans()
