@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--decode-iters", type=int, default=50)
+    ap.add_argument("--no-decode-graph", dest="decode_graph", action="store_false")
     return ap.parse_args()
 
 
@@ -263,8 +264,10 @@ def run_gpu(args):
         for sd in (64, 128, 256, 512):
             s_loc = sd // world
             xd = torch.randn(s_loc, M, device=dev, generator=gen).to(torch.bfloat16)
+            # decode runs the layer as one CUDA graph (launch-bound sizes)
+            fwd = layer.graphed(s_loc) if args.decode_graph else layer
             for _ in range(3):
-                layer(xd)
+                fwd(xd)
             lat = []
             for _ in range(args.decode_iters):
                 if world > 1:
@@ -272,7 +275,7 @@ def run_gpu(args):
                 a0 = torch.cuda.Event(enable_timing=True)
                 a1 = torch.cuda.Event(enable_timing=True)
                 a0.record()
-                layer(xd)
+                fwd(xd)
                 a1.record()
                 a1.synchronize()
                 lat.append(a0.elapsed_time(a1))

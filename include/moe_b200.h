@@ -209,12 +209,21 @@ int moe_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap, 
                 int32_t* row_base, int32_t* seg_start, int32_t* seg_rows, int32_t* recv_rows,
                 void* stream);
 
-/* System-scope flag barrier over peer signal pads: writes `epoch` into slot
- * [rank] of every peer's pad (peer_signal: device array of world pointers)
- * and waits until my_signal[i] >= epoch for all i. Bounded: sets
+/* System-scope flag barrier over peer signal pads: epoch = *epoch_counter + 1
+ * (a device counter, so the barrier can be captured in a CUDA graph) is
+ * written into slot [rank] of every peer's pad (peer_signal: device array of
+ * world pointers); waits until my_signal[i] >= epoch for all i. Bounded: sets
  * *error_flag = 1 after ~10 s instead of hanging. */
-int moe_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank, int epoch,
-                    int* error_flag, void* stream);
+int moe_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank,
+                    int* epoch_counter, int* error_flag, void* stream);
+
+/* All-gather of n int32 per rank over peer memory fused with the barrier
+ * above: src (n) goes to slot [rank] of every peer's (world, n) array
+ * (peer_dst: device array of world pointers). Used for the per-expert counts
+ * of the EP layer, so no NCCL call sits on its data path. */
+int moe_ipc_allgather_i32(const int32_t* src, int n, int32_t* const* peer_dst, int world, int rank,
+                          int* const* peer_signal, int* my_signal, int* epoch_counter,
+                          int* error_flag, void* stream);
 
 /* Dispatch straight into the owners' receive buffers over NVLink: kept row
  * (t, j) of expert e goes to peer_recv[e / e_per_rank] at row

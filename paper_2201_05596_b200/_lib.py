@@ -58,7 +58,8 @@ SIGNATURES = {
     "moe_ipc_open_handle": (_I, [_P, _P]),
     "moe_ipc_close_handle": (_I, [_P]),
     "moe_ep_plan": (_I, [_P, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
-    "moe_ipc_barrier": (_I, [_P, _P, _I, _I, _I, _P, _P]),
+    "moe_ipc_barrier": (_I, [_P, _P, _I, _I, _P, _P, _P]),
+    "moe_ipc_allgather_i32": (_I, [_P, _I, _P, _I, _I, _P, _P, _P, _P, _P]),
     "moe_dispatch_p2p": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P,
                               _P, _P, _P]),
     "moe_grouped_gemm_bf16_combine_rows": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _P, _P, _L,

@@ -419,6 +419,13 @@ class MoeLayer:
         ph(None)
         return out
 
+    def graphed(self, S: int):
+        """This layer's forward for batches of S tokens as one CUDA graph
+        (``pipeline.GraphedForward``)."""
+        from .pipeline import GraphedForward
+
+        return GraphedForward(self, S, self.M, self.dtype, self.device)
+
     def kept_assignments(self, S: int) -> int:
         """Kept (non-dropped) assignments of the last forward of size S (host sync)."""
         return int(self._ws[S]["load"].sum().item())

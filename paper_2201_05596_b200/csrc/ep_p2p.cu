@@ -64,23 +64,78 @@ __global__ void ep_plan_kernel(const int32_t* __restrict__ counts, int world, in
   }
 }
 
+// The epoch lives in device memory (incremented here), so the barrier is
+// CUDA-graph safe: a replayed graph keeps advancing it.
 __global__ void ipc_barrier_kernel(int* const* __restrict__ peer_signal, int* my_signal, int world,
-                                   int rank, int epoch, int* error_flag) {
+                                   int rank, int* epoch_counter, int* error_flag) {
+  __shared__ int epoch_s;
   const int i = threadIdx.x;
-  if (i >= world) return;
-  int* dst = peer_signal[i] + rank;
-  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(dst), "r"(epoch) : "memory");
-  const long long t0 = clock64();
-  while (true) {
-    int v;
-    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(my_signal + i) : "memory");
-    if (v >= epoch) break;
-    if (clock64() - t0 > 20000000000LL) {  // ~10 s: report instead of hanging the GPU
-      atomicExch(error_flag, 1);
-      break;
+  if (i == 0) epoch_s = *epoch_counter + 1;
+  __syncthreads();
+  const int epoch = epoch_s;
+  if (i < world) {
+    int* dst = peer_signal[i] + rank;
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(dst), "r"(epoch) : "memory");
+    const long long t0 = clock64();
+    while (true) {
+      int v;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(my_signal + i) : "memory");
+      if (v >= epoch) break;
+      if (clock64() - t0 > 20000000000LL) {  // ~10 s: report instead of hanging the GPU
+        atomicExch(error_flag, 1);
+        break;
+      }
+      __nanosleep(64);
     }
-    __nanosleep(64);
   }
+  __syncthreads();
+  if (i == 0) *epoch_counter = epoch;
+}
+
+// All-gather of n int32 per rank over peer memory, fused with a barrier: every
+// rank writes its row into slot [rank] of every peer's (world, n) array, fences
+// at system scope, then signals and waits like ipc_barrier_kernel. Graph safe
+// (device epoch); doubles as "every rank has finished its previous step".
+__global__ void ipc_allgather_kernel(const int32_t* __restrict__ src, int n,
+                                     int32_t* const* __restrict__ peer_dst, int world, int rank,
+                                     int* const* __restrict__ peer_signal, int* my_signal,
+                                     int* epoch_counter, int* error_flag) {
+  __shared__ int epoch_s;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const int32_t v = src[i];
+    for (int p = 0; p < world; ++p) peer_dst[p][rank * n + i] = v;
+  }
+  __threadfence_system();
+  if (tid == 0) epoch_s = *epoch_counter + 1;
+  __syncthreads();
+  const int epoch = epoch_s;
+  if (tid < world) {
+    int* dst = peer_signal[tid] + rank;
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(dst), "r"(epoch) : "memory");
+    const long long t0 = clock64();
+    while (true) {
+      int v;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(my_signal + tid)
+                   : "memory");
+      if (v >= epoch) break;
+      if (clock64() - t0 > 20000000000LL) {
+        atomicExch(error_flag, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *epoch_counter = epoch;
+}
+
+int launch_ipc_allgather(const int32_t* src, int n, int32_t* const* peer_dst, int world, int rank,
+                         int* const* peer_signal, int* my_signal, int* epoch_counter,
+                         int* error_flag, cudaStream_t st) {
+  ipc_allgather_kernel<<<1, 256, 0, st>>>(src, n, peer_dst, world, rank, peer_signal, my_signal,
+                                          epoch_counter, error_flag);
+  return (int)cudaGetLastError();
 }
 
 // Source side of the return (k=1): out[t] = owner's combined row, loaded over
@@ -139,9 +194,10 @@ int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t ca
   return (int)cudaGetLastError();
 }
 
-int launch_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank, int epoch,
-                       int* error_flag, cudaStream_t st) {
-  ipc_barrier_kernel<<<1, 32, 0, st>>>(peer_signal, my_signal, world, rank, epoch, error_flag);
+int launch_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank,
+                       int* epoch_counter, int* error_flag, cudaStream_t st) {
+  ipc_barrier_kernel<<<1, 32, 0, st>>>(peer_signal, my_signal, world, rank, epoch_counter,
+                                       error_flag);
   return (int)cudaGetLastError();
 }
 
@@ -191,12 +247,21 @@ int moe_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap, 
                              recv_rows, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int moe_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank, int epoch,
-                    int* error_flag, void* stream) {
-  CHECK(world >= 1 && world <= 32 && rank >= 0 && rank < world && epoch > 0);
-  CHECK(peer_signal && my_signal && error_flag);
-  return moe::launch_ipc_barrier(peer_signal, my_signal, world, rank, epoch, error_flag,
+int moe_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank,
+                    int* epoch_counter, int* error_flag, void* stream) {
+  CHECK(world >= 1 && world <= 32 && rank >= 0 && rank < world);
+  CHECK(peer_signal && my_signal && epoch_counter && error_flag);
+  return moe::launch_ipc_barrier(peer_signal, my_signal, world, rank, epoch_counter, error_flag,
                                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+int moe_ipc_allgather_i32(const int32_t* src, int n, int32_t* const* peer_dst, int world, int rank,
+                          int* const* peer_signal, int* my_signal, int* epoch_counter,
+                          int* error_flag, void* stream) {
+  CHECK(n >= 1 && world >= 1 && world <= 32 && rank >= 0 && rank < world);
+  CHECK(src && peer_dst && peer_signal && my_signal && epoch_counter && error_flag);
+  return moe::launch_ipc_allgather(src, n, peer_dst, world, rank, peer_signal, my_signal,
+                                   epoch_counter, error_flag, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int moe_dispatch_p2p(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,

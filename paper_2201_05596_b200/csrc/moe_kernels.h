@@ -68,8 +68,11 @@ int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t ca
 int launch_pull_rows(int64_t S, int64_t row_bytes, int k, int e_per_rank, const int32_t* ids,
                      const int32_t* row_index, uint8_t* const* peer_rows, uint8_t* out,
                      cudaStream_t st);
-int launch_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank, int epoch,
-                       int* error_flag, cudaStream_t st);
+int launch_ipc_allgather(const int32_t* src, int n, int32_t* const* peer_dst, int world, int rank,
+                         int* const* peer_signal, int* my_signal, int* epoch_counter,
+                         int* error_flag, cudaStream_t st);
+int launch_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank,
+                       int* epoch_counter, int* error_flag, cudaStream_t st);
 
 int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E, int k,
                           float* logits, int32_t* ids, float* gate_probs, int32_t* local_rank,

@@ -166,7 +166,6 @@ class EPMoeLayer:
         self.transport = transport
         self._ws: dict = {}
         self._p2p: dict | None = None
-        self._epoch = 0
         self._pipe = None
         self.last_plan: ExchangePlan | None = None
 
@@ -339,6 +338,13 @@ class EPMoeLayer:
         ph(None)
         return out
 
+    def graphed(self, S: int):
+        """Forward for S local tokens as one CUDA graph (all ranks must capture
+        and replay in the same order)."""
+        from .pipeline import GraphedForward
+
+        return GraphedForward(self, S, self.M, self.dtype, self.dev)
+
     def kept_assignments(self, S: int) -> int:
         if self.transport == "p2p":
             return int(self._ws[S]["kept"].sum().item())
@@ -360,6 +366,9 @@ class EPMoeLayer:
             raise ValueError("the peer-memory transport needs the same token count on every rank")
         from .ipc import IpcRegion
 
+        if not hasattr(self, "_epoch_dev"):  # one barrier epoch per layer, shared by all S
+            self._epoch_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
         M, k = self.M, self.k
         cap = self.spec.gating.capacity(S * self.world)
         rmax = max(self.E_loc * cap, 1)
@@ -371,7 +380,8 @@ class EPMoeLayer:
         off_tok = off_recv + al(rmax * M * 2)
         off_prob = off_tok + al(rmax * 4)
         off_ret = off_prob + al(rmax * 4)
-        off_sig = off_ret + al(rmax * M * 2)
+        off_cnt = off_ret + al(rmax * M * 2)
+        off_sig = off_cnt + al(self.world * self.E * 4)
         total = off_sig + al(64 * 4)
         region = IpcRegion(total, self.group, self.dev)
         i32 = dict(dtype=torch.int32, device=self.dev)
@@ -383,6 +393,8 @@ class EPMoeLayer:
             row_prob=region.tensor(off_prob, (rmax,), torch.float32),
             ret=region.tensor(off_ret, (rmax, M), torch.bfloat16),
             signal=region.tensor(off_sig, (64,), torch.int32),
+            counts=region.tensor(off_cnt, (self.world * self.E,), torch.int32),
+            peer_cnt=region.ptr_table(off_cnt),
             peer_recv=region.ptr_table(off_recv), peer_tok=region.ptr_table(off_tok),
             peer_prob=region.ptr_table(off_prob), peer_ret=region.ptr_table(off_ret),
             peer_sig=region.ptr_table(off_sig),
@@ -397,9 +409,9 @@ class EPMoeLayer:
         return st
 
     def _barrier(self, st: dict) -> None:
-        self._epoch += 1
         _lib.call("moe_ipc_barrier", st["peer_sig"].data_ptr(), st["signal"].data_ptr(),
-                  self.world, self.rank, self._epoch, st["err"].data_ptr(), _lib.stream_ptr())
+                  self.world, self.rank, self._epoch_dev.data_ptr(), st["err"].data_ptr(),
+                  _lib.stream_ptr())
 
     def check_errors(self) -> None:
         """Raise if a peer barrier timed out (call after synchronising)."""
@@ -429,10 +441,13 @@ class EPMoeLayer:
                   ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
                   stream)
         ph("counts_allgather")
-        # also orders this step after every rank's previous step (buffer reuse)
-        dist.all_gather_into_tensor(ws["counts"], ws["totals"], group=self.group)
+        # per-expert counts to every rank over peer memory; the fused barrier also
+        # orders this step after every rank's previous step (buffer reuse)
+        _lib.call("moe_ipc_allgather_i32", ws["totals"].data_ptr(), E, st["peer_cnt"].data_ptr(),
+                  self.world, self.rank, st["peer_sig"].data_ptr(), st["signal"].data_ptr(),
+                  self._epoch_dev.data_ptr(), st["err"].data_ptr(), stream)
         ph("plan")
-        _lib.call("moe_ep_plan", ws["counts"].data_ptr(), self.world, self.rank, E, cap,
+        _lib.call("moe_ep_plan", st["counts"].data_ptr(), self.world, self.rank, E, cap,
                   st["slot_base"].data_ptr(), st["row_base"].data_ptr(),
                   st["seg_start"].data_ptr(), st["seg_rows"].data_ptr(),
                   st["recv_rows"].data_ptr(), stream)

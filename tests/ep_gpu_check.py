@@ -62,6 +62,13 @@ def run_case(S_loc, M, E, k, cf, residual, skew, seed, transport="auto"):
     if not torch.equal(got, want[lo:hi]):
         err = (got.float() - want[lo:hi].float()).abs().max().item()
         raise AssertionError(f"EP output differs from single-GPU output (max abs {err})")
+    if transport == "p2p":  # the whole EP forward (NCCL all-gather + peer barriers) as a graph
+        g = ep.graphed(S_loc)
+        for _ in range(2):
+            if not torch.equal(g(x_all[lo:hi]), want[lo:hi]):
+                raise AssertionError("graph replay of the EP layer differs")
+        torch.cuda.synchronize()
+        ep.check_errors()
     dropped = int((slots_e < 0).sum())
     return dropped
 

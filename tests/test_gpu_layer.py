@@ -294,3 +294,17 @@ def test_host_pipeline_matches_device_forward():
     for xh, oh in zip(xs, outs):
         want = layer(xh.cuda()).cpu()
         assert torch.equal(oh, want)
+
+
+@pytest.mark.parametrize("k,res", [(1, False), (2, True)])
+def test_cuda_graph_replay_matches_eager(k, res):
+    S, M, E = 300, 256, 8
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=res, gating=GatingConfig(E, k, 1.0))
+    p = rounded_params(spec, 13, torch.bfloat16)
+    layer = A.MoeLayer(spec, p, dtype=torch.bfloat16, aux_loss=True)
+    g = layer.graphed(S)
+    for i in range(3):
+        x = torch.randn(S, M, device="cuda").to(torch.bfloat16)
+        got = g(x).clone()
+        want = layer(x)
+        assert torch.equal(got, want), i
