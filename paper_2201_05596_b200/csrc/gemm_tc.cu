@@ -86,7 +86,8 @@ struct Smem {
   static constexpr int kBarOff = STAGES * kStageBytes;
   static constexpr int kBarBytes = (2 * STAGES + 4) * 8 + 16;
   static constexpr int kTileOff = kBarOff + kBarBytes;
-  static constexpr int kTotal = kTileOff + (kMaxGroups + 1) * 4 + 1024;  // +1024 align slack
+  static constexpr int kBiasOff = (kTileOff + (kMaxGroups + 1) * 4 + 127) / 128 * 128;  // 2 x BN fp32
+  static constexpr int kTotal = kBiasOff + 2 * BN * 4 + 1024;            // +1024 align slack
 };
 
 template <int BN>
@@ -325,8 +326,18 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
                               (EPI != EPI_GATE ? col_part * kChunks * 32 : 0);
 
       if constexpr (EPI != EPI_GATE) {
-        const float* bias = args.bias ? args.bias + (int64_t)w * N : nullptr;
         const bool vec_ok = (N % 8) == 0;
+        // the tile's BN bias values, staged once in smem by the epilogue warps
+        // (double-buffered by accumulator index, so one barrier per tile)
+        float* sbias = reinterpret_cast<float*>(smem + L::kBiasOff) + acc * BN;
+        {
+          const float* bias = args.bias ? args.bias + (int64_t)w * N : nullptr;
+          for (int i = (warp - 2) * 32 + lane; i < BN; i += EW * 32) {
+            const int col = nb * BN + i;
+            sbias[i] = (bias != nullptr && col < N) ? __ldg(bias + col) : 0.f;
+          }
+          named_bar_sync(2, EW * 32);
+        }
         __nv_bfloat16* drow = args.D + out_row * N;
         const __nv_bfloat16* xrow = nullptr;
         float prob = 0.f;
@@ -336,47 +347,49 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
           drow = args.out + (args.x_by_row ? out_row : tok) * N;
           xrow = args.x_resid + (args.x_by_row ? out_row : tok) * N;
         }
+        // residual row chunks (COMBINE) are prefetched one chunk ahead
+        auto load_x = [&](int c, uint4 (&xq)[4]) {
+          const int col0 = nb * BN + (col_part * kChunks + c) * 32;
+          if (valid && vec_ok && col0 + 32 <= N) {
+            const uint4* xs = reinterpret_cast<const uint4*>(xrow + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              xq[q] = args.stream_hint ? ld_global_nc_hint(xs + q, pol_stream) : __ldg(xs + q);
+          }
+        };
+        uint4 xbuf[2][4];
+        if constexpr (EPI == EPI_BIAS_COMBINE) load_x(0, xbuf[0]);
         // TMEM loads double-buffered across 32-column chunks: the load of
         // chunk c+1 is in flight while chunk c is biased, activated and stored.
         uint32_t r[2][32];
         tmem_ld_32x32b_x32(t_addr, r[0]);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
-          const int col0 = nb * BN + (col_part * kChunks + c) * 32;
-          float bv[32];
-          if (bias != nullptr && vec_ok && col0 + 32 <= N) {
-            const float4* b4 = reinterpret_cast<const float4*>(bias + col0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 t4 = __ldg(b4 + q);
-              bv[4 * q] = t4.x; bv[4 * q + 1] = t4.y; bv[4 * q + 2] = t4.z; bv[4 * q + 3] = t4.w;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              bv[i] = (bias != nullptr && col0 + i < N) ? __ldg(bias + col0 + i) : 0.f;
-          }
-          uint4 xq[4];
+          const int cl = (col_part * kChunks + c) * 32;  // column inside the tile
+          const int col0 = nb * BN + cl;
           if constexpr (EPI == EPI_BIAS_COMBINE) {
-            if (valid && vec_ok && col0 + 32 <= N) {
-              const uint4* xs = reinterpret_cast<const uint4*>(xrow + col0);
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                xq[q] = args.stream_hint ? ld_global_nc_hint(xs + q, pol_stream) : __ldg(xs + q);
-            }
+            if (c + 1 < kChunks) load_x(c + 1, xbuf[(c + 1) & 1]);
           }
           tmem_ld_wait_regs(r[c & 1]);
           if (c + 1 < kChunks) tmem_ld_32x32b_x32(t_addr + (c + 1) * 32, r[(c + 1) & 1]);
           if (!valid || col0 >= N) continue;
           float v[32];
+          const float4* b4 = reinterpret_cast<const float4*>(sbias + cl);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            v[i] = __uint_as_float(r[c & 1][i]) + bv[i];
-            if constexpr (EPI == EPI_BIAS_GELU) v[i] = gelu_tanh_fast(v[i]);
+          for (int q = 0; q < 8; ++q) {
+            const float4 bq = b4[q];
+            v[4 * q + 0] = __uint_as_float(r[c & 1][4 * q + 0]) + bq.x;
+            v[4 * q + 1] = __uint_as_float(r[c & 1][4 * q + 1]) + bq.y;
+            v[4 * q + 2] = __uint_as_float(r[c & 1][4 * q + 2]) + bq.z;
+            v[4 * q + 3] = __uint_as_float(r[c & 1][4 * q + 3]) + bq.w;
+          }
+          if constexpr (EPI == EPI_BIAS_GELU) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = gelu_tanh_fast(v[i]);
           }
           if constexpr (EPI == EPI_BIAS_COMBINE) {
             if (vec_ok && col0 + 32 <= N) {
-              const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(xq);
+              const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(xbuf[c & 1]);
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = fmaf(prob, v[i], __bfloat162float(xb[i]));
             } else {
