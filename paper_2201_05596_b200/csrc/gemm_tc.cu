@@ -72,6 +72,7 @@ struct GemmArgs {
   int x_by_row;
   int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
   int raster;       // tile order (see tile_at)
+  int prefetch;     // L2 prefetch of the next tile's streamed operand
 };
 
 // CG = 1: one CTA computes a BM x BN tile (tcgen05.mma.cta_group::1, M=128).
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
     const int num_kb = (args.K + BK - 1) / BK;
     // (L2 eviction-priority hints on A/B were measured and removed: evict_first
     // on the weights raised DRAM traffic from 6.2 to 9.1 GB per GEMM1 launch)
+    int gp = 0;  // group cursor for the prefetch look-ahead
     for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int mb, nb;
       decode(tile, g, mb, nb);
@@ -215,6 +217,26 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
       const int w = args.weight_idx ? args.weight_idx[g] : g;
       const int a_row = (int)(rs + (int64_t)mb * TM + cta * BM);
       const int b_row = w * args.N + nb * BN + cta * (BN / CG);
+      if (args.prefetch && lane == 0) {
+        // Warm L2 with the NEXT tile's streamed operand while this one runs: the
+        // smem ring alone keeps too few DRAM bytes in flight per SM to hide the
+        // loaded HBM latency (x for the gate, the weights for the expert GEMMs).
+        const int nt = tile_at(it + 1);
+        if (nt < total_tiles) {
+          int pm, pn;
+          if (gp < g) gp = g;
+          decode(nt, gp, pm, pn);
+          if (EPI == EPI_GATE) {
+            const int64_t prs = args.row_start ? args.row_start[gp] : (int64_t)gp * args.row_stride;
+            const int pa = (int)(prs + (int64_t)pm * TM + cta * BM);
+            for (int kb = 0; kb < num_kb; ++kb) tma_prefetch_l2_2d(&map_a, kb * BK, pa);
+          } else {
+            const int pw = args.weight_idx ? args.weight_idx[gp] : gp;
+            const int pb = pw * args.N + pn * BN + cta * (BN / CG);
+            for (int kb = 0; kb < num_kb; ++kb) tma_prefetch_l2_2d(&map_b, kb * BK, pb);
+          }
+        }
+      }
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
@@ -605,6 +627,17 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t co
   return r == CUDA_SUCCESS ? 0 : MOE_ETMA;
 }
 
+// MOE_PREFETCH bit 0: gate GEMM prefetches the next tile's x; bit 1: expert
+// GEMMs prefetch the next tile's weights. Tuning knob, default off: measured on
+// B200 the gate did not speed up and the expert GEMMs slowed by 10-30%.
+static int prefetch_mode() {
+  static const int m = [] {
+    const char* v = getenv("MOE_PREFETCH");
+    return v ? atoi(v) : 0;
+  }();
+  return m;
+}
+
 static int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -696,6 +729,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.x_by_row = x_by_row;
   a.stream_hint = stream_hint;
   a.raster = raster;
+  a.prefetch = prefetch_mode() & 2 ? 1 : 0;
   const int64_t nblk = (N + BN - 1) / BN;
   const int64_t tm = (int64_t)BM * CG;
   const int64_t max_tiles = (int64_t)G * ((max_group_rows + tm - 1) / tm) * nblk;
@@ -757,6 +791,7 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   a.local_rank = local_rank;
   a.tile_counts = tile_counts;
   a.probsum = probsum;
+  a.prefetch = prefetch_mode() & 1 ? 1 : 0;
   const int64_t tiles = (S + BM - 1) / BM;
   switch (BN) {
     case 32: return launch_tc<32, 8, EPI_GATE>(ma, mb, a, tiles, st);
