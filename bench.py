@@ -66,7 +66,7 @@ def parse():
 # CPU reference arm (oracle port of moekit.arch.forward_layer)
 # ---------------------------------------------------------------------------
 
-CPU_SAMPLE = dict(S=4096, M=2048, E=8, k=1, cf=1.0)  # 8 experts x cap 512 of the C3 expert shape
+CPU_SAMPLE = dict(S=2048, M=2048, E=4, k=1, cf=1.0)  # 4 experts x cap 512 of the C3 expert shape
 
 
 def cpu_reference_step(state=None):
@@ -108,7 +108,11 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C3 expert shape, CPU-bounded sample", **CPU_SAMPLE},
+        "config": {"workload": WORKLOADS["c3"]["desc"], "tokens_per_gpu": WORKLOADS["c3"]["S"],
+                   "global_batch": WORKLOADS["c3"]["S"] * args.gpus, "parallelism": "cpu",
+                   "sample": {"tokens": CPU_SAMPLE["S"], "experts": CPU_SAMPLE["E"],
+                              "note": "bounded sample of the same layer shape (per-expert load "
+                                      "= the C3 capacity 512); tokens/s is per token either way"}},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": cpu_desc()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
