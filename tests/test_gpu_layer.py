@@ -308,3 +308,26 @@ def test_cuda_graph_replay_matches_eager(k, res):
         got = g(x).clone()
         want = layer(x)
         assert torch.equal(got, want), i
+
+
+@pytest.mark.parametrize("E,k,cf,M", [(3, 1, 1.0, 64), (7, 2, 0.9, 128), (96, 1, 1.5, 256),
+                                      (2, 2, 1.0, 32), (256, 1, 1.0, 128), (33, 2, 2.0, 64)])
+def test_bf16_odd_expert_counts(E, k, cf, M):
+    """Non power-of-two / tiny / maximal E on the tcgen05 gate (Epad padding)."""
+    S = 1500
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, k, cf))
+    p = rounded_params(spec, E * 7 + k, torch.bfloat16)
+    x64 = torch.randn(S, M, generator=torch.Generator().manual_seed(E)).to(torch.bfloat16).double().numpy()
+    layer, x, out, logits = run_layer(spec, p, x64, torch.bfloat16)
+    lg, _ = check_routing(layer, logits, spec, S)
+    ex, sh = oracle_args(p)
+    want = O.forward_layer_with_logits(x64, lg, ex, sh, E, k, cf)
+    close(out.float().cpu().numpy(), want, 2e-2)
+
+
+def test_bf16_limits_raise():
+    spec = A.LayerSpec(kind="moe", hidden=64, experts=300, gating=GatingConfig(300, 1, 1.0))
+    p = A.init_layer_params(A.LayerSpec(kind="moe", hidden=8, experts=2, gating=GatingConfig(2)),
+                            np.random.default_rng(0))
+    with pytest.raises((ValueError, A.ShapeError)):
+        A.MoeLayer(spec, p, dtype=torch.bfloat16)
