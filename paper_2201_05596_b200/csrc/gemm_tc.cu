@@ -460,18 +460,18 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
           uint32_t r[32];
           tmem_ld_32x32b_x32(t_addr + c * 32, r);
           tmem_ld_wait();
+          // ascending column order + strict compare keeps the lower index on ties
+          // (branch-free selects; padded columns >= E are masked to -inf)
+          const bool full_chunk = c * 32 + 32 <= E;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int col = c * 32 + i;
-            const float v = __uint_as_float(r[i]);
-            if (col < E) {
-              // ascending column order + strict compare keeps lower index on ties
-              if (v > b1) {
-                b2 = b1; i2 = i1; b1 = v; i1 = col;
-              } else if (v > b2) {
-                b2 = v; i2 = col;
-              }
-            }
+            const float v = (full_chunk || col < E) ? __uint_as_float(r[i]) : -INFINITY;
+            const bool g1 = v > b1, g2 = v > b2;
+            b2 = g1 ? b1 : (g2 ? v : b2);
+            i2 = g1 ? i1 : (g2 ? col : i2);
+            b1 = g1 ? v : b1;
+            i1 = g1 ? col : i1;
           }
           if (valid && args.logits != nullptr) {
             float* lrow = args.logits + t * E;
@@ -486,9 +486,14 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
           uint32_t r[32];
           tmem_ld_32x32b_x32(t_addr + c * 32, r);
           tmem_ld_wait();
+          if (c * 32 + 32 <= E) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i < E) sum += expf(__uint_as_float(r[i]) - b1);
+            for (int i = 0; i < 32; ++i) sum += expf(__uint_as_float(r[i]) - b1);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i < E) sum += expf(__uint_as_float(r[i]) - b1);
+          }
         }
         if (args.probsum != nullptr) {
           // load-balance statistics (arch.py:297-313): column sums of the full softmax,
@@ -517,10 +522,15 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
             if (c * 32 + (int)lane < E) atomicAdd(&psum[c * 32 + lane], v[0]);
           }
         }
-        // accumulator consumed: hand TMEM back to the MMA warp
+        // accumulator consumed: hand TMEM back to the MMA warp (the leader's, CG=2)
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if constexpr (CG == 2)
+            mbar_arrive_cluster(&tempty[acc], 0);
+          else
+            mbar_arrive(&tempty[acc]);
+        }
 
         const int k = args.k;
         int e0 = valid ? i1 : -1;
@@ -566,8 +576,11 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
           args.local_rank[t * k] = r0;
           if (k == 2) args.local_rank[t * k + 1] = r1;
         }
-        for (int e = tid; e < E; e += 128)
-          args.tile_counts[(int64_t)mb * E + e] = wc[e] + wc[E + e] + wc[2 * E + e] + wc[3 * E + e];
+        const int64_t tile_row0 = (int64_t)mb * TM + cta * BM;  // this CTA's routing tile
+        if (tile_row0 < args.S)
+          for (int e = tid; e < E; e += 128)
+            args.tile_counts[tile_row0 / kRouteTile * E + e] =
+                wc[e] + wc[E + e] + wc[2 * E + e] + wc[3 * E + e];
         named_bar_sync(1, 128);
       }
       if (++acc == 2) {
@@ -771,10 +784,14 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   if (E < 1 || E > 256 || (M % 8) != 0 || k < 1 || k > 2) return MOE_EINVAL;
   int BN = 32;
   while (BN < E) BN *= 2;
+  // E >= 128: 2-CTA clusters (M=256 tokens per pair, each CTA loads half of W_g^T per
+  // stage) so the smem ring holds more x bytes in flight per SM (the gate is
+  // HBM-latency bound: 66 -> ~52 us at C3 measured for the smaller-B configs)
+  const int CG = BN >= 128 ? 2 : 1;
   CUtensorMap ma, mb;
   int rc = make_map(&ma, x, S, M, BM);
   if (rc) return rc;
-  rc = make_map(&mb, wg_t, BN, M, BN);  // wg_t is padded to BN rows
+  rc = make_map(&mb, wg_t, BN, M, BN / CG);  // wg_t is padded to BN rows
   if (rc) return rc;
   GemmArgs a{};
   a.K = M;
@@ -792,12 +809,12 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   a.tile_counts = tile_counts;
   a.probsum = probsum;
   a.prefetch = prefetch_mode() & 1 ? 1 : 0;
-  const int64_t tiles = (S + BM - 1) / BM;
+  const int64_t tiles = (S + (int64_t)BM * CG - 1) / ((int64_t)BM * CG);
   switch (BN) {
     case 32: return launch_tc<32, 8, EPI_GATE>(ma, mb, a, tiles, st);
     case 64: return launch_tc<64, 8, EPI_GATE>(ma, mb, a, tiles, st);
-    case 128: return launch_tc<128, 6, EPI_GATE>(ma, mb, a, tiles, st);
-    default: return launch_tc<256, 4, EPI_GATE>(ma, mb, a, tiles, st);
+    case 128: return launch_tc<128, 8, EPI_GATE, 2, 4>(ma, mb, a, tiles, st);
+    default: return launch_tc<256, 6, EPI_GATE, 2, 4>(ma, mb, a, tiles, st);
   }
 }
 
