@@ -1,2 +1,1 @@
-python tools/combine_bench.py
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
+timeout 600 python -m pytest tests/test_gpu_train.py -x -q -p no:cacheprovider 2>&1 | tail -25

@@ -40,7 +40,7 @@ extern "C" {
 #define MOE_ROUTE_TILE 128 /* tokens per routing tile */
 
 enum { MOE_F32 = 0, MOE_BF16 = 1, MOE_F64 = 2 };
-enum { MOE_ACT_NONE = 0, MOE_ACT_GELU = 1 };
+enum { MOE_ACT_NONE = 0, MOE_ACT_GELU = 1, MOE_ACT_GELU_SAVE = 3, MOE_ACT_GELU_BWD = 4 };
 
 int moe_abi_version(void);
 
@@ -183,6 +183,46 @@ int moe_grouped_gemm_f32(const float* A, int K, const float* B, int N, const flo
                          int num_groups, const int32_t* row_start, int64_t row_stride,
                          const int32_t* rows, int64_t rows_const, const int32_t* weight_idx,
                          int64_t max_group_rows, int act, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Backward of the layer (training; the reference forward is tape-aware,
+ * arch.py:375-377: gradients flow through the gate probabilities that scale
+ * each expert's contribution, not through the routing decisions). bf16.
+ * ------------------------------------------------------------------------- */
+
+/* Training variants of the grouped GEMM: act = MOE_ACT_GELU_SAVE stores the
+ * pre-activation a = A@B^T + bias into aux (same shape as D) and D = gelu(a);
+ * act = MOE_ACT_GELU_BWD computes D = (A@B^T) * gelu'(aux) (aux = a). */
+int moe_grouped_gemm_bf16_aux(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
+                              int N, const float* bias, void* D, int num_groups,
+                              const int32_t* row_start, int64_t row_stride, const int32_t* rows,
+                              int64_t rows_const, const int32_t* weight_idx,
+                              int64_t max_group_rows, int act, void* aux, void* stream);
+
+/* Through the combine (mul + take_elems vjps): for each kept (t, j) with
+ * expert-buffer row r = ids*cap + slot: dy[r] = gate_prob * dout[t] (bf16)
+ * and dp[t, j] = <dout[t], y[r]> (f32, 0 for dropped). */
+int moe_combine_bwd_bf16(const void* dout, const void* y, int64_t S, int M, int E, int k,
+                         int64_t cap, const int32_t* ids, const int32_t* slots,
+                         const float* gate_probs, void* dy, float* dp, void* stream);
+
+/* Through the gate softmax (row_softmax vjp, tensor.py:263-266):
+ * dlogits[t] = s_t * (g_t - <g_t, s_t>) with s = softmax(logits[t]) and g
+ * nonzero only at the kept choices (g[ids[t,j]] = dp[t,j]); bf16 (S, Epad). */
+int moe_gate_bwd(const float* logits, int64_t S, int E, int Epad, int k, const int32_t* ids,
+                 const int32_t* slots, const float* dp, void* dlogits, void* stream);
+
+/* Per-group transpose into zero-padded K-major operands for the weight-gradient
+ * GEMMs: XT[g] (W, ldt) = X[g*row_stride : +rows[g]]^T, zero in columns
+ * >= rows[g]; colsum[g] (W, f32, nullable, caller zero-fills) += column sums. */
+int moe_transpose_rows_bf16(const void* X, int W, int num_groups, int64_t row_stride,
+                            const int32_t* rows, int64_t rows_const, int64_t ldt, void* XT,
+                            float* colsum, void* stream);
+
+/* dx[t] = dout[t] + sum_j kept dxr[ids*cap + slot] + extra1[t] (+ extra2[t]). */
+int moe_bwd_dx_bf16(const void* dout, const void* dxr, int64_t S, int M, int E, int k, int64_t cap,
+                    const int32_t* ids, const int32_t* slots, const void* extra1,
+                    const void* extra2, void* dx, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Expert parallelism over NVLink peer memory (one process per GPU of a box).

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(HERE, "libmoe_b200.so")
 
 MOE_F32, MOE_BF16, MOE_F64 = 0, 1, 2
 MOE_ACT_NONE, MOE_ACT_GELU = 0, 1
+MOE_ACT_GELU_SAVE, MOE_ACT_GELU_BWD = 3, 4
 ROUTE_TILE = 128
 MOE_EINVAL = -22
 
@@ -65,6 +66,12 @@ SIGNATURES = {
     "moe_grouped_gemm_bf16_combine_rows": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _P, _P, _L,
                                                 _P, _P, _P, _P, _P]),
     "moe_pull_rows_p2p": (_I, [_L, _L, _I, _I, _P, _P, _I, _P, _P, _P]),
+    "moe_grouped_gemm_bf16_aux": (_I, [_P, _L, _I, _P, _L, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L,
+                                       _I, _P, _P]),
+    "moe_combine_bwd_bf16": (_I, [_P, _P, _L, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
+    "moe_gate_bwd": (_I, [_P, _L, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "moe_transpose_rows_bf16": (_I, [_P, _I, _I, _L, _P, _L, _L, _P, _P, _P]),
+    "moe_bwd_dx_bf16": (_I, [_P, _P, _L, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
     "moe_grouped_gemm_f32": (_I, [_P, _I, _P, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L, _I, _P]),
 }
 

@@ -419,6 +419,20 @@ class MoeLayer:
         ph(None)
         return out
 
+    def forward_train(self, x: torch.Tensor) -> torch.Tensor:
+        """Forward keeping the backward context (bf16; ``train.forward_train``)."""
+        from .train import forward_train
+
+        return forward_train(self, x)
+
+    def backward(self, dout: torch.Tensor) -> dict:
+        """Gradients of sum(out * dout) w.r.t. x and every parameter for the last
+        ``forward_train`` (``train.backward``), in the reference layouts."""
+        from .train import backward
+
+        self.grads = backward(self, dout)
+        return self.grads
+
     def graphed(self, S: int):
         """This layer's forward for batches of S tokens as one CUDA graph
         (``pipeline.GraphedForward``)."""

@@ -1,0 +1,252 @@
+// Backward of the MoE layer forward, bf16 device path.
+//
+// The reference forward is tape-aware (arch.py:375-377): gradients flow through
+// the gate probabilities that scale each expert's contribution (row_softmax,
+// tensor.py:254-268, and take_elems, :271-292), not through the routing
+// decisions. With out = x + sum_kept p_te * y_e(x_t) [+ shared(x)]:
+//   dY_e[row]   = p * dOut[t]                         (mul vjp, tensor.py:191-207)
+//   dp[t, j]    = <dOut[t], y_e[row]>                  (take_elems vjp)
+//   dlogits[t]  = s_t * (g_t - <g_t, s_t>)            (row_softmax vjp, tensor.py:263-266)
+//   dx[t]       = dOut[t] + sum_j dX_e[row] + dlogits[t] @ W_g^T [+ shared]
+// The GEMMs run on the tcgen05 grouped kernel; weight gradients contract over
+// the token dimension, so their operands are first transposed per expert into
+// zero-padded K-major buffers (transpose_rows_kernel, which also emits the
+// bias-gradient column sums).
+#include "common.cuh"
+#include "moe_kernels.h"
+
+namespace moe {
+
+// warp per token: dY rows (bf16) for kept assignments and dp (fp32)
+__global__ void combine_bwd_kernel(const __nv_bfloat16* __restrict__ dout,
+                                   const __nv_bfloat16* __restrict__ y, int64_t S, int M, int k,
+                                   int64_t cap, const int32_t* __restrict__ ids,
+                                   const int32_t* __restrict__ slots,
+                                   const float* __restrict__ gp, __nv_bfloat16* __restrict__ dy,
+                                   float* __restrict__ dp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
+       t += warps_total) {
+    const __nv_bfloat16* g = dout + t * M;
+    for (int j = 0; j < k; ++j) {
+      const int s = slots[t * k + j];
+      if (s < 0) {
+        if (lane == 0) dp[t * k + j] = 0.f;
+        continue;
+      }
+      const int64_t row = (int64_t)ids[t * k + j] * cap + s;
+      const float p = gp[t * k + j];
+      const __nv_bfloat16* yr = y + row * M;
+      __nv_bfloat16* dr = dy + row * M;
+      float acc = 0.f;
+      for (int c = lane * 2; c < M; c += 64) {  // M even
+        const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(g + c);
+        const __nv_bfloat162 y2 = *reinterpret_cast<const __nv_bfloat162*>(yr + c);
+        const float g0 = __low2float(g2), g1 = __high2float(g2);
+        acc = fmaf(g0, __low2float(y2), acc);
+        acc = fmaf(g1, __high2float(y2), acc);
+        *reinterpret_cast<__nv_bfloat162*>(dr + c) = __floats2bfloat162_rn(p * g0, p * g1);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) dp[t * k + j] = acc;
+    }
+  }
+}
+
+// warp per token: dlogits = s * (g - <g, s>), g sparse at the kept choices.
+// Output bf16 (S, Epad), zero in the padding columns.
+__global__ void gate_bwd_kernel(const float* __restrict__ logits, int64_t S, int E, int Epad,
+                                int k, const int32_t* __restrict__ ids,
+                                const int32_t* __restrict__ slots, const float* __restrict__ dp,
+                                __nv_bfloat16* __restrict__ dlogits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
+       t += warps_total) {
+    const float* lr = logits + t * E;
+    float m = -INFINITY;
+    for (int e = lane; e < E; e += 32) m = fmaxf(m, lr[e]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    float sum = 0.f;
+    for (int e = lane; e < E; e += 32) sum += expf(lr[e] - m);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    const float inv = 1.f / sum;
+    // <g, s> over the k kept choices
+    int ej[2] = {-1, -1};
+    float gj[2] = {0.f, 0.f};
+    float dot = 0.f;
+    for (int j = 0; j < k; ++j) {
+      if (slots[t * k + j] >= 0) {
+        ej[j] = ids[t * k + j];
+        gj[j] = dp[t * k + j];
+        dot += gj[j] * expf(lr[ej[j]] - m) * inv;
+      }
+    }
+    for (int e = lane; e < Epad; e += 32) {
+      float v = 0.f;
+      if (e < E) {
+        const float se = expf(lr[e] - m) * inv;
+        const float ge = (e == ej[0] ? gj[0] : 0.f) + (e == ej[1] ? gj[1] : 0.f);
+        v = se * (ge - dot);
+      }
+      dlogits[t * Epad + e] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
+// XT[g] (W x ldt) = transpose of X rows [g*row_stride, +rows_g) (zero beyond rows_g,
+// up to ldt); optional colsum[g][c] += sum of those rows (fp32, bias gradients).
+__global__ void transpose_rows_kernel(const __nv_bfloat16* __restrict__ X, int W,
+                                      int64_t row_stride, const int32_t* __restrict__ rows,
+                                      int64_t rows_const, int64_t ldt, __nv_bfloat16* __restrict__ XT,
+                                      float* __restrict__ colsum) {
+  __shared__ float tile[32][33];
+  const int g = blockIdx.z;
+  const int64_t rg = rows ? rows[g] : rows_const;
+  const int c0 = blockIdx.x * 32;        // column of X = row of XT
+  const int64_t r0 = (int64_t)blockIdx.y * 32;  // row of X = column of XT
+  if (r0 >= ldt) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  const __nv_bfloat16* Xg = X + (int64_t)g * row_stride * W;
+  float csum = 0.f;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = r0 + i;
+    const int c = c0 + tx;
+    float v = 0.f;
+    if (r < rg && c < W) v = __bfloat162float(Xg[r * W + c]);
+    tile[i][tx] = v;
+    csum += v;
+  }
+  if (colsum != nullptr && c0 + tx < W) atomicAdd(&colsum[(int64_t)g * W + c0 + tx], csum);
+  __syncthreads();
+  __nv_bfloat16* XTg = XT + (int64_t)g * W * ldt;
+  for (int i = ty; i < 32; i += 8) {
+    const int c = c0 + i;
+    const int64_t r = r0 + tx;
+    if (c < W && r < ldt) XTg[(int64_t)c * ldt + r] = __float2bfloat16_rn(tile[tx][i]);
+  }
+}
+
+// dx[t] = dout[t] + sum_j kept dXr[row_j] + extra1[t] (+ extra2[t])
+__global__ void bwd_dx_kernel(const __nv_bfloat16* __restrict__ dout,
+                              const __nv_bfloat16* __restrict__ dxr, int64_t S, int M, int k,
+                              int64_t cap, const int32_t* __restrict__ ids,
+                              const int32_t* __restrict__ slots,
+                              const __nv_bfloat16* __restrict__ extra1,
+                              const __nv_bfloat16* __restrict__ extra2,
+                              __nv_bfloat16* __restrict__ dx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
+       t += warps_total) {
+    int64_t rr[2] = {-1, -1};
+    for (int j = 0; j < k; ++j) {
+      const int s = slots[t * k + j];
+      if (s >= 0) rr[j] = (int64_t)ids[t * k + j] * cap + s;
+    }
+    for (int c = lane * 2; c < M; c += 64) {
+      float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + t * M + c));
+      for (int j = 0; j < 2; ++j) {
+        if (rr[j] >= 0) {
+          const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dxr + rr[j] * M + c));
+          v.x += a.x;
+          v.y += a.y;
+        }
+      }
+      if (extra1) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(extra1 + t * M + c));
+        v.x += a.x;
+        v.y += a.y;
+      }
+      if (extra2) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(extra2 + t * M + c));
+        v.x += a.x;
+        v.y += a.y;
+      }
+      *reinterpret_cast<__nv_bfloat162*>(dx + t * M + c) = __floats2bfloat162_rn(v.x, v.y);
+    }
+  }
+}
+
+static int grid_warps(int64_t S) {
+  int64_t g = (S + 7) / 8;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace moe
+
+#define CHECK(cond)                 \
+  do {                              \
+    if (!(cond)) return MOE_EINVAL; \
+  } while (0)
+
+extern "C" {
+
+int moe_combine_bwd_bf16(const void* dout, const void* y, int64_t S, int M, int E, int k,
+                         int64_t cap, const int32_t* ids, const int32_t* slots,
+                         const float* gate_probs, void* dy, float* dp, void* stream) {
+  CHECK(S >= 0 && M >= 2 && M % 2 == 0 && E >= 1 && (k == 1 || k == 2) && cap >= 0);
+  if (S == 0) return MOE_OK;
+  CHECK(dout && ids && slots && gate_probs && dp && (cap == 0 || (y && dy)));
+  moe::combine_bwd_kernel<<<moe::grid_warps(S), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (const __nv_bfloat16*)dout, (const __nv_bfloat16*)y, S, M, k, cap, ids, slots, gate_probs,
+      (__nv_bfloat16*)dy, dp);
+  return (int)cudaGetLastError();
+}
+
+int moe_gate_bwd(const float* logits, int64_t S, int E, int Epad, int k, const int32_t* ids,
+                 const int32_t* slots, const float* dp, void* dlogits, void* stream) {
+  CHECK(S >= 0 && E >= 1 && Epad >= E && (k == 1 || k == 2));
+  if (S == 0) return MOE_OK;
+  CHECK(logits && ids && slots && dp && dlogits);
+  moe::gate_bwd_kernel<<<moe::grid_warps(S), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      logits, S, E, Epad, k, ids, slots, dp, (__nv_bfloat16*)dlogits);
+  return (int)cudaGetLastError();
+}
+
+int moe_transpose_rows_bf16(const void* X, int W, int num_groups, int64_t row_stride,
+                            const int32_t* rows, int64_t rows_const, int64_t ldt, void* XT,
+                            float* colsum, void* stream) {
+  CHECK(W >= 1 && num_groups >= 1 && row_stride >= 0 && ldt >= 1 && rows_const >= 0);
+  CHECK(X && XT);
+  dim3 grid((W + 31) / 32, (unsigned)((ldt + 31) / 32), num_groups);
+  moe::transpose_rows_kernel<<<grid, dim3(32, 8), 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (const __nv_bfloat16*)X, W, row_stride, rows, rows_const, ldt, (__nv_bfloat16*)XT, colsum);
+  return (int)cudaGetLastError();
+}
+
+int moe_bwd_dx_bf16(const void* dout, const void* dxr, int64_t S, int M, int E, int k, int64_t cap,
+                    const int32_t* ids, const int32_t* slots, const void* extra1,
+                    const void* extra2, void* dx, void* stream) {
+  CHECK(S >= 0 && M >= 2 && M % 2 == 0 && E >= 1 && (k == 1 || k == 2) && cap >= 0);
+  if (S == 0) return MOE_OK;
+  CHECK(dout && ids && slots && dx && (cap == 0 || dxr));
+  moe::bwd_dx_kernel<<<moe::grid_warps(S), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (const __nv_bfloat16*)dout, (const __nv_bfloat16*)dxr, S, M, k, cap, ids, slots,
+      (const __nv_bfloat16*)extra1, (const __nv_bfloat16*)extra2, (__nv_bfloat16*)dx);
+  return (int)cudaGetLastError();
+}
+
+int moe_grouped_gemm_bf16_aux(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
+                              int N, const float* bias, void* D, int num_groups,
+                              const int32_t* row_start, int64_t row_stride, const int32_t* rows,
+                              int64_t rows_const, const int32_t* weight_idx,
+                              int64_t max_group_rows, int act, void* aux, void* stream) {
+  CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1);
+  CHECK(act == MOE_ACT_GELU_SAVE || act == MOE_ACT_GELU_BWD);
+  CHECK(max_group_rows >= 0 && rows_const >= 0);
+  if (a_rows == 0 || max_group_rows == 0) return MOE_OK;
+  CHECK(A && B && D && aux);
+  const int internal = act == MOE_ACT_GELU_SAVE ? 3 : 4;
+  return moe::launch_grouped_gemm_bf16(
+      A, a_rows, K, B, b_rows, N, bias, D, num_groups, row_start, row_stride, rows, rows_const,
+      weight_idx, max_group_rows, internal, reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr,
+      act == MOE_ACT_GELU_BWD ? aux : nullptr, act == MOE_ACT_GELU_SAVE ? aux : nullptr, 0);
+}
+
+}  // extern "C"

@@ -320,6 +320,22 @@ MOE_DEV float gelu_tanh_fast(float x) {
   return fmaf(hx, tanh_fast(inner), hx);
 }
 
+// d/dx of the tanh-form GELU (the vjp of tensor.py:229-233)
+MOE_DEV float gelu_tanh_grad_fast(float x) {
+  const float c = 0.7978845608028654f;
+  const float x2 = x * x;
+  const float th = tanh_fast(c * fmaf(0.044715f * x2, x, x));
+  const float sech2 = fmaf(-th, th, 1.0f);
+  return fmaf(0.5f, 1.0f + th, 0.5f * x * sech2 * c * fmaf(3.0f * 0.044715f, x2, 1.0f));
+}
+
+MOE_DEV float gelu_tanh_grad_accurate(float x) {
+  const float c = 0.7978845608028654f;
+  const float x2 = x * x;
+  const float th = tanhf(c * (x + 0.044715f * x2 * x));
+  return 0.5f * (1.0f + th) + 0.5f * x * (1.0f - th * th) * c * (1.0f + 3.0f * 0.044715f * x2);
+}
+
 MOE_DEV uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

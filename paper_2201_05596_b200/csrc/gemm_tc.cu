@@ -28,7 +28,11 @@ namespace moe {
 
 // EPI_BIAS_COMBINE (GEMM2 of a k=1 layer): out[token(row)] = x[token] + p(row) * (acc + b2),
 // i.e. combine_tokens + the residual add of arch.py:389 fused into the epilogue.
-enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2, EPI_BIAS_COMBINE = 3 };
+// Training epilogues (layer backward):
+//   EPI_GELU_SAVE: as EPI_BIAS_GELU, also storing the pre-activation a = acc + b1 to `out`
+//   EPI_GELU_BWD : D = acc * gelu'(a), a read from `x_resid` at the same row (dA = dH * gelu'(a))
+enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2, EPI_BIAS_COMBINE = 3, EPI_GELU_SAVE = 4,
+       EPI_GELU_BWD = 5 };
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
@@ -363,12 +367,16 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
         __nv_bfloat16* drow = args.D + out_row * N;
         const __nv_bfloat16* xrow = nullptr;
         float prob = 0.f;
+        __nv_bfloat16* arow = nullptr;  // EPI_GELU_SAVE: pre-activation output row
         if constexpr (EPI == EPI_BIAS_COMBINE) {
           const int64_t tok = valid ? args.row_token[out_row] : 0;
           prob = valid ? args.row_prob[out_row] : 0.f;
           drow = args.out + (args.x_by_row ? out_row : tok) * N;
           xrow = args.x_resid + (args.x_by_row ? out_row : tok) * N;
         }
+        if constexpr (EPI == EPI_GELU_BWD) xrow = args.x_resid + out_row * N;
+        if constexpr (EPI == EPI_GELU_SAVE) arow = args.out + out_row * N;
+        constexpr bool kLoadX = EPI == EPI_BIAS_COMBINE || EPI == EPI_GELU_BWD;
         // residual row chunks (COMBINE) are prefetched one chunk ahead
         auto load_x = [&](int c, uint4 (&xq)[4]) {
           const int col0 = nb * BN + (col_part * kChunks + c) * 32;
@@ -380,7 +388,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
           }
         };
         uint4 xbuf[2][4];
-        if constexpr (EPI == EPI_BIAS_COMBINE) load_x(0, xbuf[0]);
+        if constexpr (kLoadX) load_x(0, xbuf[0]);
         // TMEM loads double-buffered across 32-column chunks: the load of
         // chunk c+1 is in flight while chunk c is biased, activated and stored.
         uint32_t r[2][32];
@@ -389,7 +397,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
         for (int c = 0; c < kChunks; ++c) {
           const int cl = (col_part * kChunks + c) * 32;  // column inside the tile
           const int col0 = nb * BN + cl;
-          if constexpr (EPI == EPI_BIAS_COMBINE) {
+          if constexpr (kLoadX) {
             if (c + 1 < kChunks) load_x(c + 1, xbuf[(c + 1) & 1]);
           }
           tmem_ld_wait_regs(r[c & 1]);
@@ -405,9 +413,41 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
             v[4 * q + 2] = __uint_as_float(r[c & 1][4 * q + 2]) + bq.z;
             v[4 * q + 3] = __uint_as_float(r[c & 1][4 * q + 3]) + bq.w;
           }
-          if constexpr (EPI == EPI_BIAS_GELU) {
+          if constexpr (EPI == EPI_GELU_SAVE) {
+            if (vec_ok && col0 + 32 <= N) {
+              uint4* ad = reinterpret_cast<uint4*>(arow + col0);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint4 pk;
+                pk.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                ad[q] = pk;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (col0 + i < N) arow[col0 + i] = __float2bfloat16_rn(v[i]);
+            }
+          }
+          if constexpr (EPI == EPI_BIAS_GELU || EPI == EPI_GELU_SAVE) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = gelu_tanh_fast(v[i]);
+          }
+          if constexpr (EPI == EPI_GELU_BWD) {  // no bias: D = dH, times gelu'(a)
+            if (vec_ok && col0 + 32 <= N) {
+              const __nv_bfloat16* ab = reinterpret_cast<const __nv_bfloat16*>(xbuf[c & 1]);
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                v[i] = __uint_as_float(r[c & 1][i]) * gelu_tanh_grad_fast(__bfloat162float(ab[i]));
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (col0 + i < N)
+                  v[i] = __uint_as_float(r[c & 1][i]) *
+                         gelu_tanh_grad_fast(__bfloat162float(xrow[col0 + i]));
+            }
           }
           if constexpr (EPI == EPI_BIAS_COMBINE) {
             if (vec_ok && col0 + 32 <= N) {
@@ -748,6 +788,26 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   const int64_t max_tiles = (int64_t)G * ((max_group_rows + tm - 1) / tm) * nblk;
   if (max_tiles == 0) return 0;
   const bool gelu = act == 1;
+  if (act == 3 || act == 4) {  // training: GELU saving the pre-activation / GELU backward
+    const bool save = act == 3;
+    if (CG == 2)
+      return save ? launch_tc<256, 6, EPI_GELU_SAVE, 2, 8>(ma, mb, a, max_tiles, st)
+                  : launch_tc<256, 6, EPI_GELU_BWD, 2, 8>(ma, mb, a, max_tiles, st);
+    switch (BN) {
+      case 32:
+        return save ? launch_tc<32, 8, EPI_GELU_SAVE, 1, 4>(ma, mb, a, max_tiles, st)
+                    : launch_tc<32, 8, EPI_GELU_BWD, 1, 4>(ma, mb, a, max_tiles, st);
+      case 64:
+        return save ? launch_tc<64, 8, EPI_GELU_SAVE, 1, 8>(ma, mb, a, max_tiles, st)
+                    : launch_tc<64, 8, EPI_GELU_BWD, 1, 8>(ma, mb, a, max_tiles, st);
+      case 128:
+        return save ? launch_tc<128, 6, EPI_GELU_SAVE, 1, 8>(ma, mb, a, max_tiles, st)
+                    : launch_tc<128, 6, EPI_GELU_BWD, 1, 8>(ma, mb, a, max_tiles, st);
+      default:
+        return save ? launch_tc<256, 4, EPI_GELU_SAVE, 1, 4>(ma, mb, a, max_tiles, st)
+                    : launch_tc<256, 4, EPI_GELU_BWD, 1, 4>(ma, mb, a, max_tiles, st);
+    }
+  }
   if (act == 2) {  // fused combine epilogue
     if (CG == 2) return launch_tc<256, 6, EPI_BIAS_COMBINE, 2, 8>(ma, mb, a, max_tiles, st);
     switch (BN) {

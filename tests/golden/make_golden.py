@@ -226,7 +226,65 @@ def route_bench():
         print("wrote", name)
 
 
+def layer_grads():
+    """Reference tape backward of loss = sum(forward_layer(x) * G) (arch.py:372-413,
+    tensor.py GradTape): gradients w.r.t. x, gate_w, every expert's w1/b1/w2/b2 and
+    the shared MLP. Inputs are bf16-representable so a bf16 device path sees them
+    exactly."""
+    from moekit.tensor import GradTape, Tensor, mul, sum_all
+
+    def bf(a):
+        a = np.asarray(a, dtype=np.float32)
+        u = a.view(np.uint32).astype(np.uint64)
+        u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000  # round-to-nearest-even to bf16
+        return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+    out = {}
+    cases = [(256, 64, 8, 1, 1.0, False, 1), (256, 64, 8, 2, 1.25, True, 2),
+             (200, 32, 4, 2, 0.6, False, 3), (300, 64, 8, 1, 0.5, True, 4)]
+    for i, (s, m, e, k, cf, res, seed) in enumerate(cases):
+        spec = LayerSpec(kind="moe", hidden=m, experts=e, residual=res,
+                         gating=gating.GatingConfig(num_experts=e, k=k, capacity_factor=cf))
+        rng = np.random.default_rng(100 + seed)
+        params = init_layer_params(spec, rng)
+        ffns = list(params.experts) + ([params.shared] if params.shared else [])
+        params.gate_w.value[:] = bf(params.gate_w.value)
+        for f in ffns:
+            f.w1.value[:] = bf(f.w1.value)
+            f.w2.value[:] = bf(f.w2.value)
+            f.b1.value[:] = np.float32(rng.standard_normal(f.b1.value.shape) * 0.05)
+            f.b2.value[:] = np.float32(rng.standard_normal(f.b2.value.shape) * 0.05)
+        x = bf(rng.standard_normal((s, m)))
+        g = rng.standard_normal((s, m))
+        tape = GradTape()
+        xt = Tensor(x, tape)
+        y = forward_layer(xt, spec, params)
+        tape.backward(sum_all(mul(y, Tensor(g))))
+        out[f"g{i}_cfg"] = np.array([s, m, e, k, cf, float(res)])
+        out[f"g{i}_x"] = x
+        out[f"g{i}_G"] = g
+        out[f"g{i}_out"] = y.value
+        out[f"g{i}_gate_w"] = params.gate_w.value
+        out[f"g{i}_dx"] = xt.grad
+        out[f"g{i}_dgate_w"] = params.gate_w.grad
+        for n in ("w1", "b1", "w2", "b2"):
+            out[f"g{i}_{n}"] = np.stack([getattr(f, n).value for f in params.experts])
+            out[f"g{i}_d{n}"] = np.stack([
+                getattr(f, n).grad if getattr(f, n).grad is not None
+                else np.zeros_like(getattr(f, n).value) for f in params.experts])
+            if res:
+                sh = params.shared
+                out[f"g{i}_s{n}"] = getattr(sh, n).value
+                out[f"g{i}_ds{n}"] = getattr(sh, n).grad
+    out["n"] = np.array(len(cases))
+    # float32 is exact for the bf16 inputs and ample for bf16-tolerance gradients
+    out = {kk: (v.astype(np.float32) if v.dtype == np.float64 and not kk.endswith("_cfg") else v)
+           for kk, v in out.items()}
+    _save("layer_grads.npz", **out)
+
+
 if __name__ == "__main__":
+    layer_grads()
     route_bench()
     gate_kats()
     scans()
