@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--decode-iters", type=int, default=50)
+    ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--no-decode-graph", dest="decode_graph", action="store_false")
     return ap.parse_args()
 
@@ -287,6 +288,29 @@ def run_gpu(args):
             if world > 1:
                 dist.all_reduce(lt, op=dist.ReduceOp.MAX)
             decode[str(sd)] = round(float(lt.median().item()), 4)
+    # ---- training step (forward saving context + backward), N=1 only: reported
+    # beside the inference metric; 12*A*M*F GEMM flops per step
+    train = None
+    if world == 1 and args.train_steps > 0 and hasattr(layer, "forward_train"):
+        gy = torch.randn(S, M, device=dev, generator=gen).to(torch.bfloat16)
+        for _ in range(2):
+            layer.forward_train(x)
+            layer.backward(gy)
+        torch.cuda.synchronize()
+        b0 = torch.cuda.Event(enable_timing=True)
+        b1 = torch.cuda.Event(enable_timing=True)
+        b0.record()
+        for _ in range(args.train_steps):
+            layer.forward_train(x)
+            layer.backward(gy)
+        b1.record()
+        torch.cuda.synchronize()
+        tms = b0.elapsed_time(b1) / args.train_steps
+        train = {"ms_per_step": round(tms, 3), "tokens_per_s": S / (tms * 1e-3),
+                 "gemm_tflops": 12.0 * kept * M * F / (tms * 1e-3) / 1e12,
+                 "steps": args.train_steps, "note": "forward_train + backward, bf16"}
+        layer._train_ctx = None
+        torch.cuda.empty_cache()
     # ---- e2e through the public API: pinned host x -> layer(x) -> pinned host out.
     # Each step uploads its 268 MB batch and downloads its 268 MB result; the
     # layer streams host batches (H2D / forward / D2H overlapped across steps).
@@ -353,6 +377,7 @@ def run_gpu(args):
                      "frac_of_burst": achieved / tf_burst if achieved else None},
         "phases_ms": phases,
         "decode_p50_ms": decode or None,
+        "train_step": train,
         "kept_assignments_per_gpu": kept_rank,
         "cpu_baseline": cpu,
         "e2e": {"value": S * world / (e2e_ms * 1e-3), "unit": UNIT,

@@ -208,9 +208,10 @@ int moe_combine_bwd_bf16(const void* dout, const void* y, int64_t S, int M, int 
 
 /* Through the gate softmax (row_softmax vjp, tensor.py:263-266):
  * dlogits[t] = s_t * (g_t - <g_t, s_t>) with s = softmax(logits[t]) and g
- * nonzero only at the kept choices (g[ids[t,j]] = dp[t,j]); bf16 (S, Epad). */
+ * nonzero only at the kept choices (g[ids[t,j]] = dp[t,j]); bf16 (S, Epad), or
+ * with split = 1 bf16 (S, 2*Epad) rows [hi | lo], hi + lo = dlogits to ~2^-16. */
 int moe_gate_bwd(const float* logits, int64_t S, int E, int Epad, int k, const int32_t* ids,
-                 const int32_t* slots, const float* dp, void* dlogits, void* stream);
+                 const int32_t* slots, const float* dp, void* dlogits, int split, void* stream);
 
 /* Per-group transpose into zero-padded K-major operands for the weight-gradient
  * GEMMs: XT[g] (W, ldt) = X[g*row_stride : +rows[g]]^T, zero in columns

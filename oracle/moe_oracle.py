@@ -309,3 +309,61 @@ def init_layer_params(hidden, num_experts, residual, rng, scale=0.1):
     experts = [ffn() for _ in range(num_experts)]
     shared = ffn() if residual else None
     return gate_w, experts, shared
+
+
+def gelu_grad(x):
+    """d gelu / dx, the vjp of tensor.py:229-233."""
+    th = np.tanh(GELU_C * (x + 0.044715 * x**3))
+    return 0.5 * (1.0 + th) + 0.5 * x * (1.0 - th**2) * GELU_C * (1.0 + 3 * 0.044715 * x**2)
+
+
+def forward_layer_backward(x, logits, gate_w, experts, shared, num_experts, k, capacity_factor,
+                           dout):
+    """Gradients of sum(forward_layer(x) * dout), the reference tape's semantics
+    (arch.py:372-413 recorded on tensor.py's GradTape): routing is constant;
+    the gate gradient flows through row_softmax (tensor.py:263-266) at the
+    kept (token, expert) pairs (take_elems vjp, :286-290); experts through
+    forward_ffn's matmul/add/gelu vjps; the skip and shared MLP add directly.
+    Returns dict(x, gate_w, w1, b1, w2, b2 (lists per expert), shared)."""
+    x = np.asarray(x, dtype=np.float64)
+    dout = np.asarray(dout, dtype=np.float64)
+    ids, _, probs = top_k_gate(logits, num_experts, k)
+    slots, _, _ = build_dispatch_plan_fast(ids, num_experts, k, capacity_factor)
+    kept = slots != DROPPED
+    dx = dout.copy()
+    dprobs = np.zeros_like(probs)
+    out = dict(w1=[], b1=[], w2=[], b2=[])
+    for e in range(num_experts):
+        w1, b1, w2, b2 = experts[e]
+        sel = kept & (ids == e)
+        order = np.argsort(slots[sel], kind="stable")
+        tokens = np.nonzero(sel)[0][order]
+        if tokens.size == 0:
+            out["w1"].append(np.zeros_like(w1)); out["b1"].append(np.zeros_like(b1))
+            out["w2"].append(np.zeros_like(w2)); out["b2"].append(np.zeros_like(b2))
+            continue
+        rows = x[tokens]
+        a1 = rows @ w1 + b1
+        h = gelu(a1)
+        y = h @ w2 + b2
+        g = dout[tokens]
+        p = probs[tokens, e][:, None]
+        dprobs[tokens, e] += (g * y).sum(axis=1)
+        dy = g * p
+        out["w2"].append(h.T @ dy); out["b2"].append(dy.sum(axis=0, keepdims=True))
+        da = (dy @ w2.T) * gelu_grad(a1)
+        out["w1"].append(rows.T @ da); out["b1"].append(da.sum(axis=0, keepdims=True))
+        np.add.at(dx, tokens, da @ w1.T)
+    dlogits = probs * (dprobs - (dprobs * probs).sum(axis=1, keepdims=True))
+    out["gate_w"] = x.T @ dlogits
+    dx += dlogits @ np.asarray(gate_w, dtype=np.float64).T
+    if shared is not None:
+        w1, b1, w2, b2 = shared
+        a1 = x @ w1 + b1
+        h = gelu(a1)
+        da = (dout @ w2.T) * gelu_grad(a1)
+        out["shared"] = dict(w1=x.T @ da, b1=da.sum(axis=0, keepdims=True), w2=h.T @ dout,
+                             b2=dout.sum(axis=0, keepdims=True))
+        dx += da @ w1.T
+    out["x"] = dx
+    return out

@@ -56,11 +56,15 @@ __global__ void combine_bwd_kernel(const __nv_bfloat16* __restrict__ dout,
 }
 
 // warp per token: dlogits = s * (g - <g, s>), g sparse at the kept choices.
-// Output bf16 (S, Epad), zero in the padding columns.
+// Output bf16 (S, Epad), zero in the padding columns; with split, rows are
+// (2*Epad) = [hi | lo], hi + lo carrying ~16 mantissa bits: the gate term of dx
+// is a large quantity that cancels against the expert term, so one bf16
+// rounding of dlogits is visible in dx (K = 2*Epad GEMM against [Wg | Wg]).
 __global__ void gate_bwd_kernel(const float* __restrict__ logits, int64_t S, int E, int Epad,
                                 int k, const int32_t* __restrict__ ids,
                                 const int32_t* __restrict__ slots, const float* __restrict__ dp,
-                                __nv_bfloat16* __restrict__ dlogits) {
+                                __nv_bfloat16* __restrict__ dlogits, int split) {
+  const int64_t ld = split ? 2 * (int64_t)Epad : Epad;
   const int lane = threadIdx.x & 31;
   const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
@@ -93,7 +97,9 @@ __global__ void gate_bwd_kernel(const float* __restrict__ logits, int64_t S, int
         const float ge = (e == ej[0] ? gj[0] : 0.f) + (e == ej[1] ? gj[1] : 0.f);
         v = se * (ge - dot);
       }
-      dlogits[t * Epad + e] = __float2bfloat16_rn(v);
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      dlogits[t * ld + e] = hi;
+      if (split) dlogits[t * ld + Epad + e] = __float2bfloat16_rn(v - __bfloat162float(hi));
     }
   }
 }
@@ -200,12 +206,12 @@ int moe_combine_bwd_bf16(const void* dout, const void* y, int64_t S, int M, int 
 }
 
 int moe_gate_bwd(const float* logits, int64_t S, int E, int Epad, int k, const int32_t* ids,
-                 const int32_t* slots, const float* dp, void* dlogits, void* stream) {
-  CHECK(S >= 0 && E >= 1 && Epad >= E && (k == 1 || k == 2));
+                 const int32_t* slots, const float* dp, void* dlogits, int split, void* stream) {
+  CHECK(S >= 0 && E >= 1 && Epad >= E && (k == 1 || k == 2) && (split == 0 || split == 1));
   if (S == 0) return MOE_OK;
   CHECK(logits && ids && slots && dp && dlogits);
   moe::gate_bwd_kernel<<<moe::grid_warps(S), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      logits, S, E, Epad, k, ids, slots, dp, (__nv_bfloat16*)dlogits);
+      logits, S, E, Epad, k, ids, slots, dp, (__nv_bfloat16*)dlogits, split);
   return (int)cudaGetLastError();
 }
 

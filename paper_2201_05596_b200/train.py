@@ -54,12 +54,13 @@ def _transpose(x, W, G, row_stride, rows, rows_const, ldt, colsum=None):
 
 def _orig_weights(layer):
     """Reference-layout copies of the weights for the data-gradient GEMMs:
-    W1 (E*M, F), W2 (E*F, M), W_g (M, Epad) (made once, on first backward)."""
+    W1 (E*M, F), W2 (E*F, M), [W_g | W_g] (M, 2*Epad) (made once, on first backward)."""
     if getattr(layer, "_w_orig", None) is None:
         E, M, F = layer.E, layer.M, layer.F
         w1o = layer.w1.view(E, F, M).transpose(1, 2).contiguous().view(E * M, F)
         w2o = layer.w2.view(E, M, F).transpose(1, 2).contiguous().view(E * F, M)
         wgo = layer.wg.t().contiguous()  # (M, Epad), zero beyond E
+        wgo = torch.cat([wgo, wgo], dim=1).contiguous()  # (M, 2*Epad): [Wg | Wg] for hi/lo dlogits
         sh = None
         if layer.shared is not None:
             s = layer.shared
@@ -168,15 +169,16 @@ def backward(layer, dout: torch.Tensor) -> dict:
     # gate: through row_softmax into W_g and x
     epad = layer.epad
     SP = _rup(max(S, 1), 8)
-    dlog = torch.empty((max(S, 1), epad), dtype=torch.bfloat16, device=dev)
+    # dlogits as bf16 hi|lo pairs (S, 2*Epad): dx's gate term = [hi|lo] @ [Wg|Wg]^T
+    dlog = torch.empty((max(S, 1), 2 * epad), dtype=torch.bfloat16, device=dev)
     dxg = torch.zeros((S, M), dtype=torch.bfloat16, device=dev)
     dwg = torch.zeros((M, epad), dtype=torch.bfloat16, device=dev)
     if S:
         _lib.call("moe_gate_bwd", c["logits"].data_ptr(), S, E, epad, k, ids.data_ptr(),
-                  slots.data_ptr(), dp.data_ptr(), dlog.data_ptr(), st)
-        _gemm(dlog, S, epad, wgo, M, None, dxg, 1, 0, None, S, S)
+                  slots.data_ptr(), dp.data_ptr(), dlog.data_ptr(), 1, st)
+        _gemm(dlog, S, 2 * epad, wgo, M, None, dxg, 1, 0, None, S, S)
         xT = _transpose(x, M, 1, 0, None, S, SP)
-        dlT = _transpose(dlog, epad, 1, 0, None, S, SP)
+        dlT = _transpose(dlog, 2 * epad, 1, 0, None, S, SP)  # rows [0, Epad) = hi^T
         _gemm(xT, M, SP, dlT, epad, None, dwg, 1, 0, None, M, M)
     grads["gate_w"] = dwg[:, :E]
     # shared MLP (Residual-MoE)

@@ -255,7 +255,7 @@ def layer_grads():
             f.b1.value[:] = np.float32(rng.standard_normal(f.b1.value.shape) * 0.05)
             f.b2.value[:] = np.float32(rng.standard_normal(f.b2.value.shape) * 0.05)
         x = bf(rng.standard_normal((s, m)))
-        g = rng.standard_normal((s, m))
+        g = bf(rng.standard_normal((s, m)))  # bf16-exact so every consumer sees it exactly
         tape = GradTape()
         xt = Tensor(x, tape)
         y = forward_layer(xt, spec, params)

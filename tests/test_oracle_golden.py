@@ -114,3 +114,31 @@ def test_dropped_tokens_ride_skip():
     x, gw, experts, shared, e, k, cf = _layer_case(z, 4)
     out = O.forward_layer(x, gw, experts, shared, e, k, cf)
     assert np.all(out == x, axis=1).sum() >= 4
+
+
+def test_backward_oracle_matches_reference_tape():
+    """The oracle's closed-form backward against moekit's GradTape (golden)."""
+    z = _load("layer_grads.npz")
+    for i in range(int(z["n"])):
+        s, m, e, k, cf, res = z[f"g{i}_cfg"]
+        e, k = int(e), int(k)
+        f64 = lambda a: np.asarray(a, dtype=np.float64)  # noqa: E731
+        experts = [(f64(z[f"g{i}_w1"][j]), f64(z[f"g{i}_b1"][j]), f64(z[f"g{i}_w2"][j]),
+                    f64(z[f"g{i}_b2"][j])) for j in range(e)]
+        shared = None
+        if res:
+            shared = tuple(f64(z[f"g{i}_s{n}"]) for n in ("w1", "b1", "w2", "b2"))
+        x, gw = f64(z[f"g{i}_x"]), f64(z[f"g{i}_gate_w"])
+        g = O.forward_layer_backward(x, x @ gw, gw, experts, shared, e, k, float(cf),
+                                     f64(z[f"g{i}_G"]))
+        tol = lambda want: 1e-6 * (np.abs(want) + np.abs(want).max())  # float32-stored fixtures  # noqa: E731
+        for key, want in (("x", z[f"g{i}_dx"]), ("gate_w", z[f"g{i}_dgate_w"])):
+            assert np.all(np.abs(g[key] - want) <= tol(want)), (i, key)
+        for n in ("w1", "b1", "w2", "b2"):
+            want = z[f"g{i}_d{n}"]
+            got = np.stack(g[n]).reshape(want.shape)
+            assert np.all(np.abs(got - want) <= tol(want)), (i, n)
+        if res:
+            for n in ("w1", "b1", "w2", "b2"):
+                want = z[f"g{i}_ds{n}"]
+                assert np.all(np.abs(g["shared"][n].reshape(want.shape) - want) <= tol(want))
