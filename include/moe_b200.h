@@ -213,12 +213,24 @@ int moe_combine_bwd_bf16(const void* dout, const void* y, int64_t S, int M, int 
 int moe_gate_bwd(const float* logits, int64_t S, int E, int Epad, int k, const int32_t* ids,
                  const int32_t* slots, const float* dp, void* dlogits, int split, void* stream);
 
-/* Per-group transpose into zero-padded K-major operands for the weight-gradient
- * GEMMs: XT[g] (W, ldt) = X[g*row_stride : +rows[g]]^T, zero in columns
- * >= rows[g]; colsum[g] (W, f32, nullable, caller zero-fills) += column sums. */
-int moe_transpose_rows_bf16(const void* X, int W, int num_groups, int64_t row_stride,
-                            const int32_t* rows, int64_t rows_const, int64_t ldt, void* XT,
-                            float* colsum, void* stream);
+/* Bias gradients: out[g][c] += sum_{r < rows[g]} X[g*row_stride + r][c] (fp32;
+ * caller zero-fills out (num_groups, W)); X bf16 row-major width W (W % 8 == 0). */
+int moe_colsum_rows_bf16(const void* X, int W, int num_groups, int64_t row_stride,
+                         const int32_t* rows, int64_t rows_const, float* out, void* stream);
+
+/* Weight gradients straight from row-major activations (tcgen05, MN-major
+ * operands, no transposes): D[g] (P x Q, bf16) = X_g^T Y_g where X_g, Y_g are
+ * rows [g*k_stride, g*k_stride + k_rows[g]) of X (x_rows x P) and Y (x_rows x Q);
+ * k_rows nullable -> k_rows_const; groups with no rows get zeros. Rows past
+ * k_rows[g] are never used (may hold anything). P, Q multiples of 8. */
+int moe_grouped_gemm_bf16_wgrad(const void* X, int64_t x_rows, int P, const void* Y, int Q,
+                                int num_groups, int64_t k_stride, const int32_t* k_rows,
+                                int64_t k_rows_const, void* D, void* stream);
+
+/* D (P x Q, fp32) += X^T Y over all `rows` (split-K across the SMs, fp32
+ * reduction; caller zero-fills D): gate and shared-MLP weight gradients. */
+int moe_gemm_bf16_wgrad_f32(const void* X, int64_t rows, int P, const void* Y, int Q, float* D,
+                            void* stream);
 
 /* dx[t] = dout[t] + sum_j kept dxr[ids*cap + slot] + extra1[t] (+ extra2[t]). */
 int moe_bwd_dx_bf16(const void* dout, const void* dxr, int64_t S, int M, int E, int k, int64_t cap,

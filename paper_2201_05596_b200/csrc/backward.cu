@@ -8,10 +8,10 @@
 //   dp[t, j]    = <dOut[t], y_e[row]>                  (take_elems vjp)
 //   dlogits[t]  = s_t * (g_t - <g_t, s_t>)            (row_softmax vjp, tensor.py:263-266)
 //   dx[t]       = dOut[t] + sum_j dX_e[row] + dlogits[t] @ W_g^T [+ shared]
-// The GEMMs run on the tcgen05 grouped kernel; weight gradients contract over
-// the token dimension, so their operands are first transposed per expert into
-// zero-padded K-major buffers (transpose_rows_kernel, which also emits the
-// bias-gradient column sums).
+// The GEMMs run on the tcgen05 grouped kernel. Weight gradients contract over
+// the token dimension: the kernel's weight-gradient mode reads both operands
+// MN-major straight from the saved row-major activations (no transposes), with
+// K = each expert's kept rows; bias gradients are column sums (colsum_rows_kernel).
 #include "common.cuh"
 #include "moe_kernels.h"
 
@@ -104,37 +104,42 @@ __global__ void gate_bwd_kernel(const float* __restrict__ logits, int64_t S, int
   }
 }
 
-// XT[g] (W x ldt) = transpose of X rows [g*row_stride, +rows_g) (zero beyond rows_g,
-// up to ldt); optional colsum[g][c] += sum of those rows (fp32, bias gradients).
-__global__ void transpose_rows_kernel(const __nv_bfloat16* __restrict__ X, int W,
-                                      int64_t row_stride, const int32_t* __restrict__ rows,
-                                      int64_t rows_const, int64_t ldt, __nv_bfloat16* __restrict__ XT,
-                                      float* __restrict__ colsum) {
-  __shared__ float tile[32][33];
-  const int g = blockIdx.z;
+// out[g][c] += sum over rows r < rows_g of X[g*row_stride + r][c] (fp32): bias
+// gradients. Block = 32 x 8 threads over 256 columns (8 per thread, 16-B loads);
+// blockIdx.z splits the rows, one atomic per column per block.
+__global__ void colsum_rows_kernel(const __nv_bfloat16* __restrict__ X, int W, int64_t row_stride,
+                                   const int32_t* __restrict__ rows, int64_t rows_const,
+                                   float* __restrict__ out) {
+  __shared__ float part[8][256 + 4];
+  const int g = blockIdx.y;
   const int64_t rg = rows ? rows[g] : rows_const;
-  const int c0 = blockIdx.x * 32;        // column of X = row of XT
-  const int64_t r0 = (int64_t)blockIdx.y * 32;  // row of X = column of XT
-  if (r0 >= ldt) return;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  const __nv_bfloat16* Xg = X + (int64_t)g * row_stride * W;
-  float csum = 0.f;
-  for (int i = ty; i < 32; i += 8) {
-    const int64_t r = r0 + i;
-    const int c = c0 + tx;
-    float v = 0.f;
-    if (r < rg && c < W) v = __bfloat162float(Xg[r * W + c]);
-    tile[i][tx] = v;
-    csum += v;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int c = blockIdx.x * 256 + tx * 8;
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  if (c < W) {
+    const __nv_bfloat16* Xg = X + (int64_t)g * row_stride * W + c;
+    for (int64_t r = (int64_t)blockIdx.z * 8 + ty; r < rg; r += (int64_t)gridDim.z * 8) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(Xg + r * W));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        acc[2 * i] += f.x;
+        acc[2 * i + 1] += f.y;
+      }
+    }
   }
-  if (colsum != nullptr && c0 + tx < W) atomicAdd(&colsum[(int64_t)g * W + c0 + tx], csum);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) part[ty][tx * 8 + i] = acc[i];
   __syncthreads();
-  __nv_bfloat16* XTg = XT + (int64_t)g * W * ldt;
-  for (int i = ty; i < 32; i += 8) {
-    const int c = c0 + i;
-    const int64_t r = r0 + tx;
-    if (c < W && r < ldt) XTg[(int64_t)c * ldt + r] = __float2bfloat16_rn(tile[tx][i]);
-  }
+  const int j = ty * 32 + tx;  // 256 columns, one per thread
+  float v = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v += part[i][j];
+  const int col = blockIdx.x * 256 + j;
+  if (col < W && v != 0.f) atomicAdd(&out[(int64_t)g * W + col], v);
 }
 
 // dx[t] = dout[t] + sum_j kept dXr[row_j] + extra1[t] (+ extra2[t])
@@ -215,15 +220,56 @@ int moe_gate_bwd(const float* logits, int64_t S, int E, int Epad, int k, const i
   return (int)cudaGetLastError();
 }
 
-int moe_transpose_rows_bf16(const void* X, int W, int num_groups, int64_t row_stride,
-                            const int32_t* rows, int64_t rows_const, int64_t ldt, void* XT,
-                            float* colsum, void* stream) {
-  CHECK(W >= 1 && num_groups >= 1 && row_stride >= 0 && ldt >= 1 && rows_const >= 0);
-  CHECK(X && XT);
-  dim3 grid((W + 31) / 32, (unsigned)((ldt + 31) / 32), num_groups);
-  moe::transpose_rows_kernel<<<grid, dim3(32, 8), 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      (const __nv_bfloat16*)X, W, row_stride, rows, rows_const, ldt, (__nv_bfloat16*)XT, colsum);
+int moe_colsum_rows_bf16(const void* X, int W, int num_groups, int64_t row_stride,
+                         const int32_t* rows, int64_t rows_const, float* out, void* stream) {
+  CHECK(W >= 8 && W % 8 == 0 && num_groups >= 1 && num_groups <= 65535 && row_stride >= 0 &&
+        rows_const >= 0);
+  CHECK(X && out);
+  const int64_t max_rows = rows ? (row_stride > 0 ? row_stride : rows_const) : rows_const;
+  if (max_rows == 0) return MOE_OK;
+  const int nx = (W + 255) / 256;
+  int64_t splits = (4 * 148 + (int64_t)nx * num_groups - 1) / ((int64_t)nx * num_groups);
+  splits = splits < 1 ? 1 : splits;
+  const int64_t by_rows = (max_rows + 63) / 64;
+  if (splits > by_rows) splits = by_rows;
+  if (splits > 65535) splits = 65535;
+  dim3 grid(nx, num_groups, (unsigned)splits);
+  moe::colsum_rows_kernel<<<grid, dim3(32, 8), 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (const __nv_bfloat16*)X, W, row_stride, rows, rows_const, out);
   return (int)cudaGetLastError();
+}
+
+int moe_grouped_gemm_bf16_wgrad(const void* X, int64_t x_rows, int P, const void* Y, int Q,
+                                int num_groups, int64_t k_stride, const int32_t* k_rows,
+                                int64_t k_rows_const, void* D, void* stream) {
+  CHECK(x_rows >= 0 && P >= 8 && P % 8 == 0 && Q >= 8 && Q % 8 == 0 && num_groups >= 1 &&
+        k_stride >= 0 && k_rows_const >= 0);
+  CHECK(D && (x_rows == 0 || (X && Y)));
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  if (x_rows == 0)
+    return (int)cudaMemsetAsync(D, 0, (size_t)num_groups * P * Q * 2, st);
+  return moe::launch_wgrad_bf16(X, x_rows, P, Y, Q, num_groups, k_stride, k_rows, k_rows_const, D,
+                                0, st);
+}
+
+int moe_gemm_bf16_wgrad_f32(const void* X, int64_t rows, int P, const void* Y, int Q, float* D,
+                            void* stream) {
+  CHECK(rows >= 0 && P >= 8 && P % 8 == 0 && Q >= 8 && Q % 8 == 0);
+  CHECK(D && (rows == 0 || (X && Y)));
+  if (rows == 0) return MOE_OK;
+  // split K (the token rows) so the (P x Q) output tiles times the splits fill the SMs
+  const int tm = Q <= 128 ? 128 : 256, bn = Q <= 128 ? 128 : 256;
+  const int64_t tiles = (int64_t)((P + tm - 1) / tm) * ((Q + bn - 1) / bn);
+  const int64_t ctas_per_tile = tm / 128;
+  int64_t splits = (148 / ctas_per_tile + tiles - 1) / tiles;
+  const int64_t max_splits = (rows + 255) / 256;
+  if (splits > max_splits) splits = max_splits;
+  if (splits < 1) splits = 1;
+  const int64_t chunk = ((rows + splits - 1) / splits + 63) / 64 * 64;
+  const int G = (int)((rows + chunk - 1) / chunk);
+  // the last chunk reads past `rows`: TMA zero-fills out-of-bounds rows
+  return moe::launch_wgrad_bf16(X, rows, P, Y, Q, G, chunk, nullptr, chunk, D, 1,
+                                reinterpret_cast<cudaStream_t>(stream));
 }
 
 int moe_bwd_dx_bf16(const void* dout, const void* dxr, int64_t S, int M, int E, int k, int64_t cap,

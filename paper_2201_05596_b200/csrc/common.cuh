@@ -176,6 +176,11 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N) {
          | ((M >> 4) << 24);      // M >> 4
 }
 
+// MN-major A and B (bits 15/16 "transpose"): the weight-gradient GEMMs
+__host__ __device__ constexpr uint32_t make_idesc_bf16_mn(uint32_t M, uint32_t N) {
+  return make_idesc_bf16(M, N) | (1u << 15) | (1u << 16);
+}
+
 // Shared-memory matrix descriptor, K-major, 128B swizzle: 8-row x 128B atoms,
 // stride between 8-row groups (SBO) = 1024 B, LBO unused (0), version 1.
 MOE_DEV uint64_t make_sdesc_sw128(const void* smem_ptr) {
@@ -187,6 +192,64 @@ MOE_DEV uint64_t make_sdesc_sw128(const void* smem_ptr) {
   d |= static_cast<uint64_t>(1u) << 46;             // version (sm_100)
   d |= static_cast<uint64_t>(2u) << 61;             // SWIZZLE_128B
   return d;
+}
+
+// Shared-memory matrix descriptor, MN-major, 128B swizzle (the weight-gradient
+// operands: X^T with X row-major, so the M/N index is the contiguous one).
+// A box of 64 MN elements x 64 K rows lands as 64 lines of 128 B (one K row per
+// line, chunks swizzled inside the line); canonical layout
+// ((64 el, m atoms), (8 rows, k groups)) : ((1, LBO), (128 B, SBO)) with
+// LBO = 8192 B between 64-element MN atoms (the next box) and SBO = 1024 B
+// between 8-row K groups. One K=16 MMA step = 2 K groups = +2048 B (>>4 -> +128).
+MOE_DEV uint64_t make_sdesc_sw128_mn(const void* smem_ptr) {
+  const uint32_t addr = smem_u32(smem_ptr);
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(8192u >> 4) << 16;     // LBO: MN atom stride
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;     // SBO: 8-row K group stride
+  d |= static_cast<uint64_t>(1u) << 46;             // version (sm_100)
+  d |= static_cast<uint64_t>(2u) << 61;             // SWIZZLE_128B
+  return d;
+}
+
+// TMA tensor store smem -> global (3-D box), tracked by bulk async-groups
+MOE_DEV void tma_store_3d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1,
+                          int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+MOE_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N committed bulk groups still read their smem source
+template <int N>
+MOE_DEV void bulk_wait_group_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+MOE_DEV void bulk_wait_group_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// generic-proxy smem writes -> visible to the async proxy (tensor core / TMA)
+MOE_DEV void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// arrive on CTA `cta`'s copy of `bar` with release at cluster scope (orders this
+// CTA's prior smem writes before the peer's wait)
+MOE_DEV void mbar_arrive_cluster_release(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+
+// fire-and-forget vector fp32 add to global memory (16-byte aligned)
+MOE_DEV void red_add_v4_f32(float* dst, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
 }
 
 // 32 lanes x 32 columns of 32-bit from TMEM into 32 registers per thread.

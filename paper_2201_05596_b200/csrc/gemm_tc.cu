@@ -31,8 +31,12 @@ namespace moe {
 // Training epilogues (layer backward):
 //   EPI_GELU_SAVE: as EPI_BIAS_GELU, also storing the pre-activation a = acc + b1 to `out`
 //   EPI_GELU_BWD : D = acc * gelu'(a), a read from `x_resid` at the same row (dA = dH * gelu'(a))
+// Weight-gradient mode (both operands MN-major, K = token rows of the group):
+//   EPI_WGRAD    : D[g] (P x N, bf16) = X_g^T Y_g, X_g / Y_g the first k_rows[g] rows
+//                  of group g (rows [g*k_stride, +k_rows[g]) of X and Y)
+//   EPI_WGRAD_ACC: Dacc (P x N, fp32) += X_g^T Y_g for every g (split-K over groups)
 enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2, EPI_BIAS_COMBINE = 3, EPI_GELU_SAVE = 4,
-       EPI_GELU_BWD = 5 };
+       EPI_GELU_BWD = 5, EPI_WGRAD = 6, EPI_WGRAD_ACC = 7 };
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
@@ -40,9 +44,10 @@ constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 // GEMMs use 8 epilogue warps (2 per TMEM lane quarter, each owning half of the
 // tile's columns) so two warps per scheduler hide the epilogue's latencies;
 // the gate epilogue (thread = token, full row of logits) uses 4.
-template <int EW>
+// (+1 fix-up warp in the weight-gradient modes: see the partial K block)
+template <int EW, int EPI = EPI_BIAS>
 constexpr int threads_for() {
-  return 64 + 32 * EW;
+  return 64 + 32 * EW + ((EPI == EPI_WGRAD || EPI == EPI_WGRAD_ACC) ? 32 : 0);
 }
 constexpr int kMaxGroups = 2048;
 
@@ -74,6 +79,11 @@ struct GemmArgs {
   // row is stored at the same row of `out` (receive layout); the source rank then
   // pulls it over NVLink
   int x_by_row;
+  // weight-gradient mode: K extent (token rows) and row base of each group
+  const int32_t* k_rows;      // [G] or null -> k_rows_const
+  int64_t k_rows_const;
+  int64_t k_stride;
+  float* Dacc;                // EPI_WGRAD_ACC output [P, N] fp32
   int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
   int raster;       // tile order (see tile_at)
   int prefetch;     // L2 prefetch of the next tile's streamed operand
@@ -83,16 +93,18 @@ struct GemmArgs {
 // CG = 2: a 2-CTA cluster computes a (2*BM) x BN tile with cta_group::2 (M=256):
 // each CTA loads its own 128 rows of A and BN/2 rows of B, the leader CTA issues
 // the MMAs for the pair, each CTA's TMEM holds its 128 accumulator rows.
-template <int BN, int STAGES, int CG>
+template <int BN, int STAGES, int CG, int OUT = 0>
 struct Smem {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOff = STAGES * kStageBytes;
-  static constexpr int kBarBytes = (2 * STAGES + 4) * 8 + 16;
+  static constexpr int kBarBytes = (3 * STAGES + 4) * 8 + 16;
   static constexpr int kTileOff = kBarOff + kBarBytes;
   static constexpr int kBiasOff = (kTileOff + (kMaxGroups + 1) * 4 + 127) / 128 * 128;  // 2 x BN fp32
-  static constexpr int kTotal = kBiasOff + 2 * BN * 4 + 1024;            // +1024 align slack
+  // epilogue staging for TMA stores (weight gradients): OUT bytes, 1024-aligned
+  static constexpr int kOutOff = (kBiasOff + 2 * BN * 4 + 1023) / 1024 * 1024;
+  static constexpr int kTotal = kOutOff + OUT + 1024;                    // +1024 align slack
 };
 
 template <int BN>
@@ -100,12 +112,24 @@ constexpr uint32_t tmem_cols() {
   return (2 * BN) < 32 ? 32 : (2 * BN);
 }
 
+// EPI_WGRAD stages each warp's 32 x 32 output chunk in smem (2 x 2 KB per warp,
+// 64-B swizzle: conflict-free row-per-lane writes) and TMA-stores it: the
+// weight-gradient tiles have a short K (one expert's tokens), so the output
+// stream is 4x denser per flop than the forward GEMMs and uncoalesced
+// row-per-thread stores became the bottleneck.
+template <int EPI, int EW>
+constexpr int out_stage_bytes() {
+  return EPI == EPI_WGRAD ? EW * 2 * 2048 : 0;
+}
+
 template <int BN, int STAGES, int EPI, int CG, int EW>
-__global__ void __launch_bounds__(threads_for<EW>(), 1)
+__global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
-  using L = Smem<BN, STAGES, CG>;
+                        const __grid_constant__ CUtensorMap map_b,
+                        const __grid_constant__ CUtensorMap map_d, GemmArgs args) {
+  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW>()>;
   constexpr int TM = BM * CG;  // rows per tile
+  constexpr bool kMN = EPI == EPI_WGRAD || EPI == EPI_WGRAD_ACC;  // MN-major operands
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -114,6 +138,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* pbar = tempty + 3;  // [STAGES] weight-gradient partial K blocks (CTA-local)
   int32_t* tile_start = reinterpret_cast<int32_t*>(smem + L::kTileOff);
 
   const uint32_t warp = warp_id_uniform();
@@ -158,6 +183,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], EW * CG);  // every epilogue warp of the pair arrives
       }
+      for (int s = 0; s < STAGES; ++s) mbar_init(&pbar[s], 1);
       mbar_fence_init();
     }
     __syncwarp();
@@ -169,6 +195,7 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
+    if constexpr (EPI == EPI_WGRAD) tma_prefetch(&map_d);
   }
   tc_fence_before();
   if constexpr (CG == 2)
@@ -241,8 +268,63 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
           }
         }
       }
-      for (int kb = 0; kb < num_kb; ++kb) {
+      int kb_end = num_kb;
+      int kg = 0;
+      if constexpr (kMN) {
+        kg = (int)(args.k_rows ? args.k_rows[g] : args.k_rows_const);
+        kb_end = (kg + BK - 1) / BK;
+      }
+      for (int kb = 0; kb < kb_end; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
+        if constexpr (kMN) {
+          // X^T / Y^T tiles: boxes of 64 MN columns x 64 token rows (one 128-B
+          // line per row); A = this CTA's BM columns of X, B = its BN/CG of Y
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          const int krow = (int)((int64_t)g * args.k_stride + (int64_t)kb * BK);
+          const int pa = mb * TM + cta * BM;
+          const int pb = nb * BN + cta * (BN / CG);
+          constexpr int kBoxB = (BN / CG) / 64;
+          const int rem = kg - kb * BK;
+          if (rem >= BK) {
+            if (lane == 0) {
+              if constexpr (CG == 2) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) tma_load_2d_cg2(sa + j * 8192, &map_a, &full[stage], pa + 64 * j, krow);
+#pragma unroll
+                for (int j = 0; j < kBoxB; ++j) tma_load_2d_cg2(sb + j * 8192, &map_b, &full[stage], pb + 64 * j, krow);
+                if (leader)
+                  mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+                else
+                  mbar_arrive_cluster(&full[stage], 0);
+              } else {
+                mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) tma_load_2d(sa + j * 8192, &map_a, &full[stage], pa + 64 * j, krow);
+#pragma unroll
+                for (int j = 0; j < kBoxB; ++j) tma_load_2d(sb + j * 8192, &map_b, &full[stage], pb + 64 * j, krow);
+              }
+            }
+          } else {
+            // last, partial K block: rows >= rem belong to padding (or the next
+            // group) and may hold anything, NaN included. Load into this CTA's smem
+            // on the stage's local barrier; the fix-up warp zeroes those rows and
+            // then releases the stage to the MMA (the producer does not stall)
+            if (lane == 0) {
+              mbar_arrive_expect_tx(&pbar[stage], L::kStageBytes);
+#pragma unroll
+              for (int j = 0; j < 2; ++j) tma_load_2d(sa + j * 8192, &map_a, &pbar[stage], pa + 64 * j, krow);
+#pragma unroll
+              for (int j = 0; j < kBoxB; ++j) tma_load_2d(sb + j * 8192, &map_b, &pbar[stage], pb + 64 * j, krow);
+            }
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
         if (lane == 0) {
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
@@ -268,31 +350,41 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only; lane 0 issues, whole warp waits)
-    constexpr uint32_t idesc = make_idesc_bf16(TM, BN);
+    constexpr uint32_t idesc = kMN ? make_idesc_bf16_mn(TM, BN) : make_idesc_bf16(TM, BN);
+    // K step of one MMA (16 elements): +32 B inside the swizzle line (K-major) or
+    // two 8-row groups (+2048 B, MN-major); descriptor units are 16 B
+    constexpr uint64_t kStep = kMN ? 128 : 2;
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     const int num_kb = (args.K + BK - 1) / BK;
+    int g = 0;
     for (int it = 0, tile = tile_at(0); leader && tile < total_tiles; tile = tile_at(++it)) {
+      int kb_end = num_kb;
+      if constexpr (kMN) {
+        int mb_, nb_;
+        decode(tile, g, mb_, nb_);
+        const int64_t kg = args.k_rows ? args.k_rows[g] : args.k_rows_const;
+        kb_end = (int)((kg + BK - 1) / BK);  // 0 for an empty group: the epilogue writes zeros
+      }
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = 0; kb < kb_end; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
           const uint8_t* sa = smem + stage * L::kStageBytes;
           const uint8_t* sb = sa + L::kABytes;
-          const uint64_t adesc = make_sdesc_sw128(sa);
-          const uint64_t bdesc = make_sdesc_sw128(sb);
+          const uint64_t adesc = kMN ? make_sdesc_sw128_mn(sa) : make_sdesc_sw128(sa);
+          const uint64_t bdesc = kMN ? make_sdesc_sw128_mn(sb) : make_sdesc_sw128(sb);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            // advance 16 bf16 = 32 B along K inside the swizzle row (>>4 -> +2)
             if constexpr (CG == 2)
-              umma_bf16_cg2(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+              umma_bf16_cg2(d_tmem, adesc + kStep * kk, bdesc + kStep * kk, idesc, (kb | kk) != 0);
             else
-              umma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+              umma_bf16(d_tmem, adesc + kStep * kk, bdesc + kStep * kk, idesc, (kb | kk) != 0);
           }
           if constexpr (CG == 2)
             umma_commit_cg2(&empty[stage], 0x3);  // frees the stage in both CTAs
@@ -317,8 +409,8 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
         acc_phase ^= 1;
       }
     }
-  } else {
-    // ===================== epilogue warps 2..5
+  } else if (warp < 2 + EW) {
+    // ===================== epilogue warps 2..2+EW-1
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
     constexpr int kColSplit = EW / 4;    // warps sharing a quarter split the columns
     const int col_part = (int)(warp - 2) / 4;          // 0 .. kColSplit-1
@@ -329,6 +421,8 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
     int g = 0;
     const int N = args.N;
     const uint64_t pol_stream = policy_evict_first();
+    int ostage = 0;  // EPI_WGRAD staging buffer toggle
+    (void)ostage;
     if constexpr (EPI == EPI_GATE) {
       if (args.probsum != nullptr) {
         float* psum = reinterpret_cast<float*>(smem + L::kTileOff) + 8 + 4 * args.E;
@@ -345,6 +439,8 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
       const int64_t local_row = (int64_t)mb * TM + row_in_tile;
       const bool valid = local_row < rows_g;
       const int64_t out_row = rs + local_row;
+      bool kzero = false;  // weight gradient of a group with no rows: zeros, TMEM not written
+      if constexpr (kMN) kzero = (args.k_rows ? args.k_rows[g] : args.k_rows_const) == 0;
 
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -402,6 +498,34 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
           }
           tmem_ld_wait_regs(r[c & 1]);
           if (c + 1 < kChunks) tmem_ld_32x32b_x32(t_addr + (c + 1) * 32, r[(c + 1) & 1]);
+          if constexpr (EPI == EPI_WGRAD) {
+            // whole warp: 32 rows x 32 columns -> smem (row = lane, 64 B) -> TMA store;
+            // rows past P / columns past N are clipped by the 3-D map (N, P, G)
+            if (col0 < N) {
+              uint8_t* ob = smem + L::kOutOff + ((warp - 2) * 2 + (ostage & 1)) * 2048;
+              if (lane == 0) bulk_wait_group_read<1>();  // this buffer's previous store has read it
+              __syncwarp();
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint4 pk;
+                const uint32_t* rr = r[c & 1] + 8 * q;
+                pk.x = kzero ? 0u : pack_bf16x2(__uint_as_float(rr[0]), __uint_as_float(rr[1]));
+                pk.y = kzero ? 0u : pack_bf16x2(__uint_as_float(rr[2]), __uint_as_float(rr[3]));
+                pk.z = kzero ? 0u : pack_bf16x2(__uint_as_float(rr[4]), __uint_as_float(rr[5]));
+                pk.w = kzero ? 0u : pack_bf16x2(__uint_as_float(rr[6]), __uint_as_float(rr[7]));
+                const int chunk = q ^ ((lane >> 1) & 3);  // SWIZZLE_64B
+                *reinterpret_cast<uint4*>(ob + lane * 64 + chunk * 16) = pk;
+              }
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(&map_d, ob, col0, (int)(mb * TM + cta * BM + quarter * 32), g);
+                bulk_commit_group();
+              }
+              ++ostage;
+            }
+            continue;
+          }
           if (!valid || col0 >= N) continue;
           float v[32];
           const float4* b4 = reinterpret_cast<const float4*>(sbias + cl);
@@ -412,6 +536,26 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
             v[4 * q + 1] = __uint_as_float(r[c & 1][4 * q + 1]) + bq.y;
             v[4 * q + 2] = __uint_as_float(r[c & 1][4 * q + 2]) + bq.z;
             v[4 * q + 3] = __uint_as_float(r[c & 1][4 * q + 3]) + bq.w;
+          }
+          if constexpr (EPI == EPI_WGRAD_ACC) {  // split-K partial: fp32 reduction in HBM/L2
+            if (kzero) continue;
+            float* dst = args.Dacc + out_row * N + col0;
+            if ((N % 4) == 0 && col0 + 32 <= N) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                red_add_v4_f32(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (col0 + i < N) atomicAdd(dst + i, v[i]);
+            }
+            continue;
+          }
+          if constexpr (EPI == EPI_WGRAD) {
+            if (kzero) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
           }
           if constexpr (EPI == EPI_GELU_SAVE) {
             if (vec_ok && col0 + 32 <= N) {
@@ -628,11 +772,58 @@ __global__ void __launch_bounds__(threads_for<EW>(), 1)
         acc_phase ^= 1;
       }
     }
+    if constexpr (EPI == EPI_WGRAD) {
+      if (lane == 0) bulk_wait_group_all();
+      __syncwarp();
+    }
     if constexpr (EPI == EPI_GATE) {
       if (args.probsum != nullptr) {  // one global atomic per expert per CTA
         named_bar_sync(1, 128);
         const float* psum = reinterpret_cast<const float*>(smem + L::kTileOff) + 8 + 4 * args.E;
         for (int i = (warp - 2) * 32 + lane; i < args.E; i += 128) atomicAdd(&args.probsum[i], psum[i]);
+      }
+    }
+  } else if constexpr (kMN) {
+    // ===================== fix-up warp (weight gradients): walks the producer's
+    // stage sequence; for each partial K block waits for its TMA, zeroes the rows
+    // >= rem (whole 128-B lines: the swizzle only permutes chunks inside a line),
+    // makes the writes visible to the tensor core and releases the stage
+    int stage = 0;
+    uint32_t pph = 0;  // per-stage parity of pbar
+    int g = 0;
+    constexpr int kBoxB = (BN / CG) / 64;
+    for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
+      int mb, nb;
+      decode(tile, g, mb, nb);
+      const int kg = (int)(args.k_rows ? args.k_rows[g] : args.k_rows_const);
+      const int kb_end = (kg + BK - 1) / BK;
+      if (kb_end > 0) {
+        stage = (stage + kb_end - 1) % STAGES;  // only the last K block can be partial
+        const int rem = kg - (kb_end - 1) * BK;
+        if (rem < BK) {
+          mbar_wait(&pbar[stage], (pph >> stage) & 1u);
+          pph ^= 1u << stage;
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+          for (int box = 0; box < 2 + kBoxB; ++box) {  // A's 2 boxes, then B's
+            uint4* base = reinterpret_cast<uint4*>(sa + box * 8192);
+            for (int i = rem * 8 + (int)lane; i < 512; i += 32) base[i] = z;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2) {
+              if (leader)
+                mbar_arrive(&full[stage]);
+              else
+                mbar_arrive_cluster_release(&full[stage], 0);
+            } else {
+              mbar_arrive(&full[stage]);
+            }
+          }
+          __syncwarp();
+        }
+        stage = (stage + 1) % STAGES;
       }
     }
   }
@@ -680,6 +871,21 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t co
   return r == CUDA_SUCCESS ? 0 : MOE_ETMA;
 }
 
+// 3-D bf16 [G][P][N] output map for the weight-gradient TMA stores: box 32 x 32 x 1,
+// 64-B swizzle (matches the epilogue's staging layout); clips at P and N.
+static int make_map_out3d(CUtensorMap* map, void* base, int64_t G, int64_t P, int64_t N) {
+  auto enc = get_encode();
+  if (!enc) return MOE_ENODRV;
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)P, (cuuint64_t)G};
+  cuuint64_t strides[2] = {(cuuint64_t)(N * 2), (cuuint64_t)(P * N * 2)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : MOE_ETMA;
+}
+
 // MOE_PREFETCH bit 0: gate GEMM prefetches the next tile's x; bit 1: expert
 // GEMMs prefetch the next tile's weights. Tuning knob, default off: measured on
 // B200 the gate did not speed up and the expert GEMMs slowed by 10-30%.
@@ -703,8 +909,8 @@ static int num_sms() {
 
 template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
-                     int64_t max_tiles, cudaStream_t st) {
-  using L = Smem<BN, STAGES, CG>;
+                     int64_t max_tiles, cudaStream_t st, const CUtensorMap* md = nullptr) {
+  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW>()>;
   auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -717,7 +923,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   grid -= grid % CG;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(threads_for<EW>());
+  cfg.blockDim = dim3(threads_for<EW, EPI>());
   cfg.dynamicSmemBytes = L::kTotal;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -727,7 +933,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, args);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, md ? *md : mb, args);
   return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
@@ -835,6 +1041,49 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                   : launch_tc<256, 4, EPI_BIAS, 1, 4>(ma, mb, a, max_tiles, st);
   }
 #undef MOE_TC
+}
+
+// Weight gradients: D = X^T Y per group (see EPI_WGRAD). X: [x_rows, P], Y:
+// [x_rows, Q] row-major bf16 (P, Q multiples of 8); K rows of group g start at
+// g * k_stride. acc = 0: D bf16 [G, P, Q]; acc = 1: D fp32 [P, Q] += sum over g.
+int launch_wgrad_bf16(const void* X, int64_t x_rows, int P, const void* Y, int Q, int G,
+                      int64_t k_stride, const int32_t* k_rows, int64_t k_rows_const, void* D,
+                      int acc, cudaStream_t st) {
+  if (G < 1 || G > kMaxGroups || P < 8 || Q < 8 || (P % 8) || (Q % 8) || x_rows < 0) return MOE_EINVAL;
+  static const int stream_hint = [] {
+    const char* v = getenv("MOE_STORE_HINT");
+    return v ? atoi(v) : 1;
+  }();
+  const int BN = Q <= 128 ? 128 : 256;
+  const int CG = BN == 256 ? 2 : 1;
+  CUtensorMap ma, mb;
+  // box = 64 columns (one 128-B swizzle line) x 64 token rows
+  int rc = make_map(&ma, X, x_rows, P, BK);
+  if (rc) return rc;
+  rc = make_map(&mb, Y, x_rows, Q, BK);
+  if (rc) return rc;
+  GemmArgs a{};
+  a.N = Q;
+  a.K = BK;
+  a.G = G;
+  a.row_stride = acc ? 0 : P;  // output rows of group g: [g*P, +P) (bf16) or all into [0, P)
+  a.rows_const = P;
+  a.k_rows = k_rows;
+  a.k_rows_const = k_rows_const;
+  a.k_stride = k_stride;
+  a.D = acc ? nullptr : (__nv_bfloat16*)D;
+  a.Dacc = acc ? (float*)D : nullptr;
+  a.stream_hint = acc ? 0 : stream_hint;
+  const int64_t tiles = (int64_t)G * ((P + BM * CG - 1) / (BM * CG)) * ((Q + BN - 1) / BN);
+  if (x_rows == 0 && acc) return 0;
+  if (acc)
+    return BN == 256 ? launch_tc<256, 6, EPI_WGRAD_ACC, 2, 8>(ma, mb, a, tiles, st)
+                     : launch_tc<128, 6, EPI_WGRAD_ACC, 1, 8>(ma, mb, a, tiles, st);
+  CUtensorMap md;
+  rc = make_map_out3d(&md, D, G, P, Q);
+  if (rc) return rc;
+  return BN == 256 ? launch_tc<256, 5, EPI_WGRAD, 2, 8>(ma, mb, a, tiles, st, &md)
+                   : launch_tc<128, 5, EPI_WGRAD, 1, 8>(ma, mb, a, tiles, st, &md);
 }
 
 int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int E, int k,

@@ -61,6 +61,10 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              const float* row_prob = nullptr, const void* x_resid = nullptr,
                              void* out = nullptr, int x_by_row = 0);
 
+int launch_wgrad_bf16(const void* X, int64_t x_rows, int P, const void* Y, int Q, int G,
+                      int64_t k_stride, const int32_t* k_rows, int64_t k_rows_const, void* D,
+                      int acc, cudaStream_t st);
+
 // expert parallelism over NVLink peer memory (ep_p2p.cu)
 int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap,
                    int32_t* slot_base, int32_t* row_base, int32_t* seg_start, int32_t* seg_rows,

@@ -28,10 +28,6 @@ import torch
 from . import _lib
 
 
-def _rup(n: int, m: int) -> int:
-    return (n + m - 1) // m * m
-
-
 def _gemm(a, a_rows, K, w, N, bias, d, G, row_stride, rows, rows_const, max_rows, act=0,
           aux=None):
     st = _lib.stream_ptr()
@@ -45,10 +41,18 @@ def _gemm(a, a_rows, K, w, N, bias, d, G, row_stride, rows, rows_const, max_rows
                   None, max_rows, act, st)
 
 
-def _transpose(x, W, G, row_stride, rows, rows_const, ldt, colsum=None):
-    out = torch.empty((G * W, ldt), dtype=torch.bfloat16, device=x.device)
-    _lib.call("moe_transpose_rows_bf16", x.data_ptr(), W, G, row_stride, _lib.ptr(rows),
-              rows_const, ldt, out.data_ptr(), _lib.ptr(colsum), _lib.stream_ptr())
+def _wgrad(x, P, y, Q, G, k_stride, k_rows, k_rows_const):
+    """bf16 (G, P, Q): X_g^T Y_g over each group's first k_rows[g] rows (no transposes)."""
+    out = torch.empty((G, P, Q), dtype=torch.bfloat16, device=x.device)
+    _lib.call("moe_grouped_gemm_bf16_wgrad", x.data_ptr(), x.shape[0], P, y.data_ptr(), Q, G,
+              k_stride, _lib.ptr(k_rows), k_rows_const, out.data_ptr(), _lib.stream_ptr())
+    return out
+
+
+def _colsum(x, W, G, row_stride, rows, rows_const):
+    out = torch.zeros((G, W), dtype=torch.float32, device=x.device)
+    _lib.call("moe_colsum_rows_bf16", x.data_ptr(), W, G, row_stride, _lib.ptr(rows), rows_const,
+              out.data_ptr(), _lib.stream_ptr())
     return out
 
 
@@ -137,7 +141,6 @@ def backward(layer, dout: torch.Tensor) -> dict:
     f32 = dict(dtype=torch.float32, device=dev)
     grads = {}
     dp = torch.zeros((S, k), **f32)
-    capP = _rup(max(cap, 1), 8)
     dxr = None
     if cap and S:
         dy = torch.empty((E * cap, M), dtype=torch.bfloat16, device=dev)
@@ -149,18 +152,13 @@ def backward(layer, dout: torch.Tensor) -> dict:
               c["a"])
         dxr = torch.empty((E * cap, M), dtype=torch.bfloat16, device=dev)
         _gemm(dA, E * cap, F, w1o, M, None, dxr, E, cap, load, 0, cap)
-        # weight gradients: contract over each expert's kept rows (K = padded capacity)
-        db2 = torch.zeros((E, M), **f32)
-        db1 = torch.zeros((E, F), **f32)
-        hT = _transpose(c["h"], F, E, cap, load, 0, capP)
-        dyT = _transpose(dy, M, E, cap, load, 0, capP, db2)
-        xT_e = _transpose(c["xbuf"], M, E, cap, load, 0, capP)
-        dAT = _transpose(dA, F, E, cap, load, 0, capP, db1)
-        dw2 = torch.empty((E * F, M), dtype=torch.bfloat16, device=dev)
-        _gemm(hT, E * F, capP, dyT, M, None, dw2, E, F, None, F, F)
-        dw1 = torch.empty((E * M, F), dtype=torch.bfloat16, device=dev)
-        _gemm(xT_e, E * M, capP, dAT, F, None, dw1, E, M, None, M, M)
-        grads.update(w1=dw1.view(E, M, F), b1=db1, w2=dw2.view(E, F, M), b2=db2)
+        # weight gradients: contract over each expert's kept rows, read MN-major
+        # straight from the saved activations
+        db2 = _colsum(dy, M, E, cap, load, 0)
+        db1 = _colsum(dA, F, E, cap, load, 0)
+        dw2 = _wgrad(c["h"], F, dy, M, E, cap, load, 0)
+        dw1 = _wgrad(c["xbuf"], M, dA, F, E, cap, load, 0)
+        grads.update(w1=dw1, b1=db1, w2=dw2, b2=db2)
     else:
         grads.update(w1=torch.zeros((E, M, F), dtype=torch.bfloat16, device=dev),
                      b1=torch.zeros((E, F), **f32),
@@ -168,19 +166,17 @@ def backward(layer, dout: torch.Tensor) -> dict:
                      b2=torch.zeros((E, M), **f32))
     # gate: through row_softmax into W_g and x
     epad = layer.epad
-    SP = _rup(max(S, 1), 8)
     # dlogits as bf16 hi|lo pairs (S, 2*Epad): dx's gate term = [hi|lo] @ [Wg|Wg]^T
     dlog = torch.empty((max(S, 1), 2 * epad), dtype=torch.bfloat16, device=dev)
-    dxg = torch.zeros((S, M), dtype=torch.bfloat16, device=dev)
-    dwg = torch.zeros((M, epad), dtype=torch.bfloat16, device=dev)
+    dxg = torch.empty((S, M), dtype=torch.bfloat16, device=dev)
+    dwg = torch.zeros((M, 2 * epad), **f32)
     if S:
         _lib.call("moe_gate_bwd", c["logits"].data_ptr(), S, E, epad, k, ids.data_ptr(),
                   slots.data_ptr(), dp.data_ptr(), dlog.data_ptr(), 1, st)
         _gemm(dlog, S, 2 * epad, wgo, M, None, dxg, 1, 0, None, S, S)
-        xT = _transpose(x, M, 1, 0, None, S, SP)
-        dlT = _transpose(dlog, 2 * epad, 1, 0, None, S, SP)  # rows [0, Epad) = hi^T
-        _gemm(xT, M, SP, dlT, epad, None, dwg, 1, 0, None, M, M)
-    grads["gate_w"] = dwg[:, :E]
+        _lib.call("moe_gemm_bf16_wgrad_f32", x.data_ptr(), S, M, dlog.data_ptr(), 2 * epad,
+                  dwg.data_ptr(), st)
+    grads["gate_w"] = dwg[:, :E] + dwg[:, epad:epad + E]  # hi + lo (fp32)
     # shared MLP (Residual-MoE)
     dxs = None
     if layer.shared is not None and S:
@@ -190,16 +186,10 @@ def backward(layer, dout: torch.Tensor) -> dict:
         _gemm(dout, S, M, s2o, F, None, dA_s, 1, 0, None, S, S, _lib.MOE_ACT_GELU_BWD, a_s)
         dxs = torch.empty((S, M), dtype=torch.bfloat16, device=dev)
         _gemm(dA_s, S, F, s1o, M, None, dxs, 1, 0, None, S, S)
-        sdb2 = torch.zeros((1, M), **f32)
-        sdb1 = torch.zeros((1, F), **f32)
-        hsT = _transpose(h_s, F, 1, 0, None, S, SP)
-        doT = _transpose(dout, M, 1, 0, None, S, SP, sdb2)
-        xT = _transpose(x, M, 1, 0, None, S, SP)
-        dAsT = _transpose(dA_s, F, 1, 0, None, S, SP, sdb1)
-        sdw2 = torch.empty((F, M), dtype=torch.bfloat16, device=dev)
-        _gemm(hsT, F, SP, doT, M, None, sdw2, 1, 0, None, F, F)
-        sdw1 = torch.empty((M, F), dtype=torch.bfloat16, device=dev)
-        _gemm(xT, M, SP, dAsT, F, None, sdw1, 1, 0, None, M, M)
+        sdb2 = _colsum(dout, M, 1, 0, None, S)
+        sdb1 = _colsum(dA_s, F, 1, 0, None, S)
+        sdw2 = _wgrad(h_s, F, dout, M, 1, 0, None, S)[0]
+        sdw1 = _wgrad(x, M, dA_s, F, 1, 0, None, S)[0]
         grads["shared"] = dict(w1=sdw1, b1=sdb1, w2=sdw2, b2=sdb2)
     dx = torch.empty_like(dout)
     if S:

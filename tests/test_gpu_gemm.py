@@ -110,3 +110,57 @@ def test_grouped_gemm_f32(K, N, act):
             want = _gelu(want)
         got = d[g * cap:g * cap + r].double()
         assert ((got - want).abs() <= 1e-5 * (want.abs() + want.abs().mean())).all()
+
+
+@pytest.mark.parametrize("P,Q", [(2048, 512), (256, 256), (64, 128), (200, 96), (512, 2048), (136, 264)])
+def test_wgrad_bf16(P, Q):
+    """Weight-gradient mode (MN-major operands): D[g] = X_g^T Y_g over each
+    group's first k_rows[g] rows; rows past k_rows hold NaN and must not leak."""
+    torch.manual_seed(P * 7 + Q)
+    G, cap = 6, 300
+    k_rows = [300, 0, 129, 1, 64, 257]
+    x = torch.randn(G * cap, P, device="cuda").to(torch.bfloat16)
+    y = torch.randn(G * cap, Q, device="cuda").to(torch.bfloat16)
+    for g, r in enumerate(k_rows):
+        x[g * cap + r:(g + 1) * cap] = float("nan")
+        y[g * cap + r:(g + 1) * cap] = float("nan")
+    kr = torch.tensor(k_rows, dtype=torch.int32, device="cuda")
+    d = torch.full((G, P, Q), 7.0, dtype=torch.bfloat16, device="cuda")
+    _lib.call("moe_grouped_gemm_bf16_wgrad", x.data_ptr(), G * cap, P, y.data_ptr(), Q, G, cap,
+              kr.data_ptr(), 0, d.data_ptr(), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    for g, r in enumerate(k_rows):
+        xs, ys = x[g * cap:g * cap + r].float(), y[g * cap:g * cap + r].float()
+        want = xs.t() @ ys
+        got = d[g].float()
+        assert torch.isfinite(got).all(), g
+        tol = 1e-2 * (want.abs() + want.abs().mean() + 1e-3)
+        assert ((got - want).abs() <= tol).all(), (g, (got - want).abs().max().item())
+
+
+@pytest.mark.parametrize("rows,P,Q", [(65536, 2048, 256), (3000, 512, 16), (100, 64, 128), (70000, 1024, 512)])
+def test_wgrad_f32_splitk(rows, P, Q):
+    torch.manual_seed(rows + P)
+    x = torch.randn(rows, P, device="cuda").to(torch.bfloat16)
+    y = torch.randn(rows, Q, device="cuda").to(torch.bfloat16)
+    d = torch.zeros(P, Q, device="cuda")
+    _lib.call("moe_gemm_bf16_wgrad_f32", x.data_ptr(), rows, P, y.data_ptr(), Q, d.data_ptr(),
+              _lib.stream_ptr())
+    want = x.double().t() @ y.double()
+    err = (d.double() - want).abs()
+    # fp32 accumulation of exact bf16 products: error ~ rows * eps32 * |x||y|
+    assert err.max().item() <= 1e-5 * rows ** 0.5 * 4 + 1e-4 * want.abs().max().item(), err.max().item()
+
+
+def test_colsum_rows():
+    torch.manual_seed(3)
+    G, cap, W = 5, 300, 1032
+    rows = [300, 0, 129, 1, 257]
+    x = torch.randn(G * cap, W, device="cuda").to(torch.bfloat16)
+    r = torch.tensor(rows, dtype=torch.int32, device="cuda")
+    out = torch.zeros(G, W, device="cuda")
+    _lib.call("moe_colsum_rows_bf16", x.data_ptr(), W, G, cap, r.data_ptr(), 0, out.data_ptr(),
+              _lib.stream_ptr())
+    for g, n in enumerate(rows):
+        want = x[g * cap:g * cap + n].double().sum(0)
+        assert torch.allclose(out[g].double(), want, atol=1e-3, rtol=1e-5), g
