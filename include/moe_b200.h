@@ -301,6 +301,12 @@ int moe_grouped_gemm_bf16_combine_rows(const void* A, int64_t a_rows, int K, con
                                        const int32_t* row_token, const float* row_prob,
                                        const void* x_rows, void* out_rows, void* stream);
 
+/* Row permutation dst[i] = src[index[i]] (i < n; row_bytes % 16 == 0): the
+ * layout transforms of the hierarchical and coordinated all-to-all schedules
+ * (commsim.py:280-464 "layout-transform" steps). */
+int moe_gather_rows(const void* src, int64_t row_bytes, const int32_t* index, int64_t n,
+                    void* dst, void* stream);
+
 /* Source side (k=1): out[t] = peer_rows[owner(ids[t])][row_index[t]] over
  * NVLink for every kept token (peer_rows: device array of world pointers). */
 int moe_pull_rows_p2p(int64_t S, int64_t row_bytes, int E, int k, const int32_t* ids,

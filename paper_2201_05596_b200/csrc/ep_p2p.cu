@@ -141,6 +141,31 @@ int launch_ipc_allgather(const int32_t* src, int n, int32_t* const* peer_dst, in
 // Source side of the return (k=1): out[t] = owner's combined row, loaded over
 // NVLink from the owner's receive-layout buffer (16 B per lane, 512 B per warp
 // access). Dropped tokens were already written (out = x) by the dispatch.
+// dst[i] = src[index[i]]: the layout transforms between the phases of the
+// hierarchical / coordinated exchanges (warp per row, 16-B vectors).
+__global__ void gather_rows_kernel(const uint4* __restrict__ src, int64_t vec_per_row,
+                                   const int32_t* __restrict__ index, int64_t n,
+                                   uint4* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+       i += warps_total) {
+    const uint4* s = src + (int64_t)index[i] * vec_per_row;
+    uint4* d = dst + i * vec_per_row;
+    for (int64_t v = lane; v < vec_per_row; v += 32) d[v] = __ldg(s + v);
+  }
+}
+
+int launch_gather_rows(const uint8_t* src, int64_t row_bytes, const int32_t* index, int64_t n,
+                       uint8_t* dst, cudaStream_t st) {
+  int64_t blocks = (n + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gather_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(src),
+                                                       row_bytes / 16, index, n,
+                                                       reinterpret_cast<uint4*>(dst));
+  return (int)cudaGetLastError();
+}
+
 template <typename V>
 __global__ void pull_rows_kernel(int64_t S, int64_t row_bytes, int k, int e_per_rank,
                                  const int32_t* __restrict__ ids,
@@ -286,6 +311,15 @@ int moe_dispatch_p2p(const void* x, int64_t S, int64_t row_bytes, int E, int k, 
   a.out_dropped = static_cast<uint8_t*>(out_dropped);
   a.row_index = row_index;
   return moe::launch_scatter(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int moe_gather_rows(const void* src, int64_t row_bytes, const int32_t* index, int64_t n,
+                    void* dst, void* stream) {
+  CHECK(row_bytes >= 16 && row_bytes % 16 == 0 && n >= 0);
+  if (n == 0) return MOE_OK;
+  CHECK(src && index && dst && src != dst);
+  return moe::launch_gather_rows(static_cast<const uint8_t*>(src), row_bytes, index, n,
+                                 static_cast<uint8_t*>(dst), reinterpret_cast<cudaStream_t>(stream));
 }
 
 int moe_pull_rows_p2p(int64_t S, int64_t row_bytes, int E, int k, const int32_t* ids,

@@ -72,6 +72,8 @@ int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t ca
 int launch_pull_rows(int64_t S, int64_t row_bytes, int k, int e_per_rank, const int32_t* ids,
                      const int32_t* row_index, uint8_t* const* peer_rows, uint8_t* out,
                      cudaStream_t st);
+int launch_gather_rows(const uint8_t* src, int64_t row_bytes, const int32_t* index, int64_t n,
+                       uint8_t* dst, cudaStream_t st);
 int launch_ipc_allgather(const int32_t* src, int n, int32_t* const* peer_dst, int world, int rank,
                          int* const* peer_signal, int* my_signal, int* epoch_counter,
                          int* error_flag, cudaStream_t st);

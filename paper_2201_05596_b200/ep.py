@@ -21,7 +21,9 @@ the source pulls its rows back with wide NVLink loads; a 2-line flag barrier
 (system-scope release/acquire) separates the phases, and the plan is computed
 on device from the all-gathered counts (no host sync).
 
-"nccl" (any k, shared MLP) - one NCCL all-to-all each way:
+"nccl" (any k, shared MLP) - one all-to-all each way, flat (one NCCL
+all_to_all_single) or, with schedule="hierarchical", the two-phase
+node/rail schedule of commsim.py:280-370 (exchange.py):
   send buffer on rank r : kept rows ordered (owner rank, expert, slot)
   receive buffer        : [source rank][local expert][rows in slot order]
                           (commsim's delivery contract: ordered by source,
@@ -29,6 +31,15 @@ on device from the all-gathered counts (no host sync).
   the grouped GEMM runs directly on the receive layout (one group per
   (source, local expert) segment), the results go back with the inverse
   all-to-all, and the combine gathers them by the row index dispatch wrote.
+
+``SlicedEPMoeLayer``: tensor-sliced groups of L ranks (planner tensor_slice,
+planner.py:160-174) that hold identical token shards; experts are block-sharded
+over the groups and each expert's FFN is sliced L ways along d_ff inside its
+group (expert slicing, planner.py:207-222 - with one expert per group this is
+the planner's latency mode for p > E). Tokens move with the coordinated
+schedule (commsim.py:373-464), the slices' partial GEMM2 outputs are summed
+with an all-reduce inside the group, and every member combines its group's
+tokens.
 """
 
 from __future__ import annotations
@@ -41,10 +52,12 @@ import torch.distributed as dist
 
 from . import _lib
 from .arch import FFN_MULT, DenseFfn, LayerSpec, MoeLayerParams, _grouped_gemm, _Phases, _t
+from .exchange import Exchanger, ReplicaMismatchError
 from .gating import GatingConfig
 from .tensor import ShapeError
 
-__all__ = ["ExchangePlan", "make_exchange_plan", "gather_counts", "exchange_rows", "EPMoeLayer"]
+__all__ = ["ExchangePlan", "make_exchange_plan", "gather_counts", "exchange_rows", "EPMoeLayer",
+           "SlicedEPMoeLayer", "rank_counts"]
 
 
 @dataclass
@@ -103,6 +116,11 @@ def make_exchange_plan(counts: np.ndarray, cap: int, rank: int, num_experts: int
                         expert_load=expert_load)
 
 
+def rank_counts(plan: ExchangePlan) -> np.ndarray:
+    """(world, world) kept rows source rank -> owner rank (the exchange's split matrix)."""
+    return plan.kept.reshape(plan.world, plan.world, plan.E_loc).sum(axis=2)
+
+
 def gather_counts(out_flat: torch.Tensor, totals: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather every rank's (E,) expert counts into a flat (world*E,) tensor."""
     dist.all_gather_into_tensor(out_flat, totals, group=group)
@@ -121,7 +139,8 @@ class EPMoeLayer:
     """One MoE layer sharded over the ranks of ``group`` (bf16, tcgen05 path)."""
 
     def __init__(self, spec: LayerSpec, gate_w, local_experts, shared=None, group=None,
-                 dtype=torch.bfloat16, device=None, transport: str = "auto") -> None:
+                 dtype=torch.bfloat16, device=None, transport: str = "auto",
+                 schedule: str = "flat", gpus_per_node: int | None = None) -> None:
         if spec.kind != "moe":
             raise ShapeError("EPMoeLayer needs a moe LayerSpec")
         if dtype != torch.bfloat16:
@@ -158,12 +177,16 @@ class EPMoeLayer:
         # memory (k=1, no shared MLP); "nccl": two all_to_all_single exchanges.
         p2p_ok = self.k == 1 and self.shared is None
         if transport == "auto":
-            transport = "p2p" if p2p_ok else "nccl"
+            transport = "p2p" if (p2p_ok and schedule == "flat") else "nccl"
+        if schedule != "flat" and transport != "nccl":
+            raise ValueError(f"schedule {schedule!r} runs on the nccl transport")
         if transport == "p2p" and not p2p_ok:
             raise ValueError("the peer-memory transport covers k=1 layers without a shared MLP")
         if transport not in ("p2p", "nccl"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
+        self.schedule = schedule
+        self.exchanger = Exchanger(group, schedule, gpus_per_node) if transport == "nccl" else None
         self._ws: dict = {}
         self._p2p: dict | None = None
         self._pipe = None
@@ -308,8 +331,8 @@ class EPMoeLayer:
                       ws["send"].data_ptr(), st)
         ph("all_to_all_dispatch")
         self._recv_buffers(ws, plan.n_recv)
-        recv = exchange_rows(ws["recv"], ws["send"], plan.recv_splits, plan.send_splits,
-                             self.group)
+        C = rank_counts(plan)
+        recv = self.exchanger.all_to_all(ws["recv"], ws["send"], C)
         n_recv = plan.n_recv
         max_rows = int(plan.seg_rows.max()) if plan.seg_rows.size else 0
         if n_recv and max_rows:
@@ -324,7 +347,7 @@ class EPMoeLayer:
                       seg_start_d.data_ptr(), 0, seg_rows_d.data_ptr(), 0, seg_w_d.data_ptr(),
                       max_rows, _lib.MOE_ACT_NONE, st)
         ph("all_to_all_return")
-        exchange_rows(ws["ret"], ws["y"], plan.send_splits, plan.recv_splits, self.group)
+        self.exchanger.all_to_all(ws["ret"], ws["y"], C.T)
         shared_out = None
         if self.shared is not None:
             ph("shared_mlp")
@@ -499,3 +522,173 @@ class EPMoeLayer:
             return ws["ids"], ws["gp"], ws["slots"], SimpleNamespace(cap=st["cap"],
                                                                      expert_load=load)
         return ws["ids"], ws["gp"], ws["slots"], self.last_plan
+
+
+class SlicedEPMoeLayer(EPMoeLayer):
+    """MoE layer over tensor-sliced groups with expert slicing (bf16, NCCL).
+
+    Ranks form Q = world / L groups of L consecutive ranks (tensor_slice L,
+    planner.py:160-174: groups never span nodes); the members of a group hold
+    the same token shard. Group q owns experts [q*E/Q, (q+1)*E/Q) and member t
+    of the group holds d_ff slice [t*F/L, (t+1)*F/L) of each of them: W1
+    columns, b1 and W2 rows of the slice (b2 on member 0), so
+      y = sum_t gelu(x W1_t + b1_t) W2_t + b2      (expert slicing, planner.py:207-222).
+    Forward: gate + global-capacity plan over the Q groups (the replicas must
+    agree - ReplicaMismatchError otherwise, commsim.py:404-411), coordinated
+    dispatch (commsim.py:373-464), per-slice GEMMs, all-reduce of the partial
+    outputs inside the group, coordinated return, combine. Routing and slots
+    equal the single-GPU layer on the concatenated group shards bit-exactly;
+    outputs differ from it only by the bf16 rounding of the slice partials."""
+
+    def __init__(self, spec: LayerSpec, gate_w, group_experts, shared=None, group=None,
+                 tensor_slice: int = 2, dtype=torch.bfloat16, device=None) -> None:
+        if spec.kind != "moe":
+            raise ShapeError("SlicedEPMoeLayer needs a moe LayerSpec")
+        if dtype != torch.bfloat16:
+            raise TypeError("the expert-parallel path is bf16 (tcgen05)")
+        if spec.residual:
+            raise ValueError("the sliced layer covers layers without the Residual-MoE shared MLP")
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        L = int(tensor_slice)
+        if L < 1 or self.world % L:
+            raise ValueError(f"tensor_slice {tensor_slice} must divide world {self.world}")
+        self.L, self.Q = L, self.world // L
+        self.q, self.t = divmod(self.rank, L)
+        E, M = spec.experts, spec.hidden
+        F = FFN_MULT * M
+        if E % self.Q:
+            raise ValueError(f"{E} experts do not divide over {self.Q} groups (planner.py:202-206)")
+        if F % L or (F // L) % 8:
+            raise ValueError(f"d_ff {F} does not slice into {L} multiples of 8")
+        dev = _lib.require_device(None) if device is None else torch.device(device)
+        self.spec, self.dev, self.dtype = spec, dev, dtype
+        self.E, self.M, self.F, self.k = E, M, F, spec.gating.k
+        self.E_loc = E // self.Q
+        self.Fs = Fs = F // L
+        if len(group_experts) != self.E_loc:
+            raise ShapeError(f"{len(group_experts)} group experts, expected {self.E_loc}")
+        gw = _t(gate_w, dev, torch.float32)
+        self.epad = max(32, 1 << (E - 1).bit_length())
+        self.wg = torch.zeros((self.epad, M), dtype=torch.bfloat16, device=dev)
+        self.wg[:E] = gw.t().to(torch.bfloat16)
+        lo, hi = self.t * Fs, (self.t + 1) * Fs
+        self.w1 = torch.empty((self.E_loc * Fs, M), dtype=torch.bfloat16, device=dev)
+        self.w2 = torch.empty((self.E_loc * M, Fs), dtype=torch.bfloat16, device=dev)
+        self.b1 = torch.empty((self.E_loc, Fs), dtype=torch.float32, device=dev)
+        self.b2 = torch.zeros((self.E_loc, M), dtype=torch.float32, device=dev)
+        for i, p in enumerate(group_experts):
+            self.w1[i * Fs:(i + 1) * Fs] = _t(p.w1, dev, torch.bfloat16)[:, lo:hi].t()
+            self.w2[i * M:(i + 1) * M] = _t(p.w2, dev, torch.bfloat16)[lo:hi].t()
+            self.b1[i] = _t(p.b1, dev, torch.float32).reshape(F)[lo:hi]
+            if self.t == 0:  # the output bias once per group
+                self.b2[i] = _t(p.b2, dev, torch.float32).reshape(M)
+        self.shared = None
+        self.transport, self.schedule = "nccl", "coordinated"
+        self.exchanger = Exchanger(group, "coordinated", tensor_slice=L)
+        self._ws: dict = {}
+        self._p2p = None
+        self._pipe = None
+        self.last_plan: ExchangePlan | None = None
+
+    @classmethod
+    def from_params(cls, spec: LayerSpec, params: MoeLayerParams, group=None, tensor_slice: int = 2,
+                    **kw):
+        """This group's expert block out of full (replicated) parameters."""
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        Q = world // tensor_slice
+        e_loc = spec.experts // Q
+        q = rank // tensor_slice
+        local = params.experts[q * e_loc:(q + 1) * e_loc]
+        return cls(spec, params.gate_w, local, params.shared, group=group,
+                   tensor_slice=tensor_slice, **kw)
+
+    def graphed(self, S: int):
+        raise NotImplementedError("the sliced layer syncs counts on the host (NCCL splits)")
+
+    def kept_assignments(self, S: int) -> int:
+        return int(self.last_plan.kept[self.q].sum()) if self.last_plan is not None else 0
+
+    def _forward_dev(self, x: torch.Tensor, out: torch.Tensor | None = None, timer=None):
+        if x.device != self.dev:
+            x = x.to(self.dev, non_blocking=True)
+        x = x.to(self.dtype).contiguous()
+        if x.dim() != 2 or x.shape[1] != self.M:
+            raise ShapeError(f"batch width {tuple(x.shape)} does not match layer hidden {self.M}")
+        S = x.shape[0]
+        out = torch.empty_like(x) if out is None else out
+        ws = self._workspace(S)
+        E, M, Fs, k, L, Q = self.E, self.M, self.Fs, self.k, self.L, self.Q
+        st = _lib.stream_ptr()
+        ph = _Phases(timer)
+        ids, gp, lr, tc = ws["ids"], ws["gp"], ws["local_rank"], ws["tile_counts"]
+        ph("gate")
+        if S:
+            _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k, None,
+                      ids.data_ptr(), gp.data_ptr(), lr.data_ptr(), tc.data_ptr(), st)
+        _lib.call("moe_plan_scan", tc.data_ptr(), S, E, 2 ** 62, None,
+                  ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
+                  st)
+        ph("counts_allgather")
+        counts = gather_counts(ws["counts"], ws["totals"], self.group).cpu().numpy()
+        counts = counts.reshape(Q, L, E)
+        if not (counts == counts[:, :1]).all():
+            raise ReplicaMismatchError("members of a tensor group routed different token shards")
+        gcounts = counts[:, 0]
+        s_total = int(gcounts.sum()) // k
+        cap = self.spec.gating.capacity(s_total)
+        plan = make_exchange_plan(gcounts, cap, self.q, E)  # groups play the ranks
+        self.last_plan = plan
+        ph("scan")
+        G = Q * self.E_loc
+        tables = np.concatenate([plan.base[self.q], plan.send_row_base, plan.seg_row_start,
+                                 plan.seg_rows, plan.seg_weight]).astype(np.int32)
+        tab = torch.from_numpy(tables).to(self.dev, non_blocking=True)
+        base_d, row_base_d = tab[:E], tab[E:2 * E]
+        seg_start_d, seg_rows_d, seg_w_d = tab[2 * E:2 * E + G], tab[2 * E + G:2 * E + 2 * G], \
+            tab[2 * E + 2 * G:2 * E + 3 * G]
+        _lib.call("moe_plan_scan", tc.data_ptr(), S, E, cap, base_d.data_ptr(),
+                  ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
+                  st)
+        ph("dispatch")
+        if S:
+            _lib.call("moe_dispatch_ep", x.data_ptr(), S, M * 2, E, k, cap, ids.data_ptr(),
+                      lr.data_ptr(), ws["tile_offsets"].data_ptr(), base_d.data_ptr(),
+                      row_base_d.data_ptr(), ws["slots"].data_ptr(), ws["row_index"].data_ptr(),
+                      ws["send"].data_ptr(), st)
+        ph("coordinated_dispatch")
+        n_recv = plan.n_recv
+        if ws.get("recv_rows", -1) < n_recv:
+            rows = max(n_recv, 1)
+            ws["recv"] = torch.empty((rows, M), dtype=self.dtype, device=self.dev)
+            ws["h"] = torch.empty((rows, Fs), dtype=self.dtype, device=self.dev)
+            ws["y"] = torch.empty((rows, M), dtype=self.dtype, device=self.dev)
+            ws["recv_rows"] = rows
+        Cg = rank_counts(plan)
+        recv = self.exchanger.coordinated(ws["recv"], ws["send"], Cg)
+        max_rows = int(plan.seg_rows.max()) if plan.seg_rows.size else 0
+        y = ws["y"][:n_recv]
+        if n_recv and max_rows:
+            ph("gemm1_slice")
+            _lib.call("moe_grouped_gemm_bf16", recv.data_ptr(), n_recv, M, self.w1.data_ptr(),
+                      self.E_loc * Fs, Fs, self.b1.data_ptr(), ws["h"].data_ptr(), G,
+                      seg_start_d.data_ptr(), 0, seg_rows_d.data_ptr(), 0, seg_w_d.data_ptr(),
+                      max_rows, _lib.MOE_ACT_GELU, st)
+            ph("gemm2_slice")
+            _lib.call("moe_grouped_gemm_bf16", ws["h"].data_ptr(), n_recv, Fs, self.w2.data_ptr(),
+                      self.E_loc * M, M, self.b2.data_ptr(), y.data_ptr(), G,
+                      seg_start_d.data_ptr(), 0, seg_rows_d.data_ptr(), 0, seg_w_d.data_ptr(),
+                      max_rows, _lib.MOE_ACT_NONE, st)
+            if L > 1:
+                ph("slice_allreduce")
+                dist.all_reduce(y, group=self.exchanger.slice_group)
+        ph("coordinated_return")
+        self.exchanger.coordinated(ws["ret"], ws["y"], Cg.T)
+        ph("combine")
+        if S:
+            _lib.call("moe_combine", ws["ret"].data_ptr(), _lib.MOE_BF16, S, M, E, k, cap,
+                      ids.data_ptr(), ws["slots"].data_ptr(), ws["row_index"].data_ptr(),
+                      gp.data_ptr(), _lib.MOE_F32, x.data_ptr(), None, out.data_ptr(), 1, st)
+        ph(None)
+        return out

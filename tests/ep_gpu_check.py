@@ -16,16 +16,11 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2201_05596_b200 import arch as A  # noqa: E402
-from paper_2201_05596_b200.ep import EPMoeLayer  # noqa: E402
+from paper_2201_05596_b200.ep import EPMoeLayer, SlicedEPMoeLayer  # noqa: E402
 from paper_2201_05596_b200.gating import GatingConfig  # noqa: E402
 
 
-def run_case(S_loc, M, E, k, cf, residual, skew, seed, transport="auto"):
-    rank, world = dist.get_rank(), dist.get_world_size()
-    dev = torch.device("cuda", torch.cuda.current_device())
-    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=residual,
-                       gating=GatingConfig(E, k, cf))
-    g = torch.Generator(device=dev).manual_seed(seed)
+def make_params(M, E, residual, skew, g, dev):
     F = 4 * M
     gw = torch.randn(M, E, device=dev, generator=g) * 0.1
     gw += torch.randn(1, E, device=dev, generator=g) * skew
@@ -38,7 +33,57 @@ def run_case(S_loc, M, E, k, cf, residual, skew, seed, transport="auto"):
         sh = A.FfnParams(torch.randn(M, F, device=dev, generator=g) * 0.1,
                          torch.zeros(1, F, device=dev), torch.randn(F, M, device=dev, generator=g) * 0.1,
                          torch.zeros(1, M, device=dev))
-    params = A.MoeLayerParams(gate_w=gw, experts=tuple(ex), shared=sh)
+    return A.MoeLayerParams(gate_w=gw, experts=tuple(ex), shared=sh)
+
+
+def run_sliced(S_grp, M, E, k, cf, skew, seed, L):
+    """Tensor-sliced groups + expert slicing vs the single-GPU layer on the
+    concatenated group shards: routing bit-exact, outputs to bf16 tolerance
+    (the slices' partial sums are rounded to bf16 before the all-reduce)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Q = world // L
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=False,
+                       gating=GatingConfig(E, k, cf))
+    g = torch.Generator(device=dev).manual_seed(seed)
+    params = make_params(M, E, False, skew, g, dev)
+    x_all = torch.randn(S_grp * Q, M, device=dev, generator=g).to(torch.bfloat16)
+    full = A.MoeLayer(spec, params, dtype=torch.bfloat16, device=dev, fuse_combine=False)
+    want = full(x_all)
+    ids_f, gp_f, slots_f, load_f, cap_f = full.plan(S_grp * Q)
+    layer = SlicedEPMoeLayer.from_params(spec, params, tensor_slice=L)
+    q = rank // L
+    lo, hi = q * S_grp, (q + 1) * S_grp
+    got = layer(x_all[lo:hi].clone())
+    got = layer(x_all[lo:hi].clone())
+    torch.cuda.synchronize()
+    ids_e, gp_e, slots_e, plan = layer.plan(S_grp)
+    assert plan.cap == cap_f
+    assert torch.equal(ids_e, ids_f[lo:hi]), "ids differ"
+    assert torch.equal(slots_e, slots_f[lo:hi]), "global slots differ"
+    e_loc = E // Q
+    assert np.array_equal(plan.expert_load, load_f[q * e_loc:(q + 1) * e_loc].cpu().numpy())
+    w = want[lo:hi].double()
+    rms = w.pow(2).mean().sqrt()
+    excess = ((got.double() - w).abs() - 2e-2 * (w.abs() + rms)).max().item()
+    assert excess <= 0, f"sliced output off by {excess}"
+    # every member of a group holds the same output
+    peers = [torch.empty_like(got) for _ in range(world)]
+    dist.all_gather(peers, got)
+    for u in range(L):
+        assert torch.equal(peers[q * L + u], got), "group members disagree"
+    st = layer.exchanger.last_stats
+    return st
+
+
+def run_case(S_loc, M, E, k, cf, residual, skew, seed, transport="auto", schedule="flat",
+             gpus_per_node=None):
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=residual,
+                       gating=GatingConfig(E, k, cf))
+    g = torch.Generator(device=dev).manual_seed(seed)
+    params = make_params(M, E, residual, skew, g, dev)
     x_all = torch.randn(S_loc * world, M, device=dev, generator=g).to(torch.bfloat16)
     # the p2p transport fuses combine into GEMM2 like the single-GPU k=1 path;
     # the nccl transport uses the separate combine kernel
@@ -46,7 +91,8 @@ def run_case(S_loc, M, E, k, cf, residual, skew, seed, transport="auto"):
                       fuse_combine=(transport == "p2p"))
     want = full(x_all)
     ids_f, gp_f, slots_f, load_f, cap_f = full.plan(S_loc * world)
-    ep = EPMoeLayer.from_params(spec, params, transport=transport)
+    ep = EPMoeLayer.from_params(spec, params, transport=transport, schedule=schedule,
+                                gpus_per_node=gpus_per_node)
     lo, hi = rank * S_loc, (rank + 1) * S_loc
     got = ep(x_all[lo:hi].clone())
     got = ep(x_all[lo:hi].clone())  # second call: buffer reuse / slot alternation
@@ -92,6 +138,24 @@ def main():
             if dist.get_rank() == 0:
                 print(f"ep ok world={world} transport={transport} case={c} "
                       f"dropped_on_rank0={dropped}", flush=True)
+    # hierarchical node/rail schedule (2 "nodes" of world/2 GPUs): bit-identical too
+    if world % 2 == 0:
+        for c in cases[:2] + cases[3:4]:
+            run_case(*c, transport="nccl", schedule="hierarchical", gpus_per_node=world // 2)
+            if dist.get_rank() == 0:
+                print(f"ep ok world={world} schedule=hierarchical G={world // 2} case={c}",
+                      flush=True)
+    # tensor-sliced groups with expert slicing (coordinated exchange)
+    sl_cases = [(2048, 1024, 8, 1, 1.0, 0.5, 11, 2), (1500, 512, 4, 2, 0.8, 1.0, 12, 2),
+                (1024, 1024, max(world // 2, 1), 1, 1.25, 0.0, 13, 2),  # p > E: one expert per group
+                (1000, 512, 8, 2, 1.0, 0.5, 14, world)]
+    for c in sl_cases:
+        if world % c[-1] or c[2] % (world // c[-1]):
+            continue
+        st = run_sliced(*c)
+        if dist.get_rank() == 0:
+            print(f"ep ok world={world} schedule=coordinated L={c[-1]} case={c} "
+                  f"rounds={st.a2a_rounds}+{st.allgather_rounds}", flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -283,7 +283,51 @@ def layer_grads():
     _save("layer_grads.npz", **out)
 
 
+def commsim_cases():
+    """The reference's exchange schedules (commsim.py:239-464) on seeded payloads:
+    per-rank send lists and the delivered receive lists, plus the trace totals."""
+    from moekit import commsim as cs
+
+    out = {}
+    cases = []
+    # (kind, world, param, per_rank, seed): param = gpus_per_node or tensor_slice
+    for seed in range(3):
+        cases.append(("hierarchical", 4, 2, 6, seed))
+    cases.append(("hierarchical", 4, 4, 5, 7))
+    cases.append(("hierarchical", 4, 1, 5, 8))
+    cases.append(("hierarchical", 2, 2, 9, 9))
+    for seed in range(3):
+        cases.append(("coordinated", 4, 2, 7, 10 + seed))
+    cases.append(("coordinated", 4, 4, 6, 20))
+    cases.append(("coordinated", 4, 1, 6, 21))
+    cases.append(("coordinated", 2, 2, 6, 22))
+    for i, (kind, world, param, per, seed) in enumerate(cases):
+        if kind == "hierarchical":
+            sends = cs.synthetic_sends(world, per, nbytes=64, seed=seed)
+            trace = cs.hierarchical_all_to_all(sends, param)
+            flat = cs.flat_all_to_all(sends)
+            assert trace.recv == flat.recv
+            out[f"c{i}_flat_volume"] = np.array(flat.volume_bytes)
+            out[f"c{i}_flat_rounds"] = np.array(flat.a2a_rounds)
+        else:
+            logical = cs.synthetic_sends(world // param, per, nbytes=64, seed=seed)
+            sends = [list(items) for items in logical for _ in range(param)]
+            trace = cs.coordinated_all_to_all(sends, param)
+        out[f"c{i}_cfg"] = np.array([0 if kind == "hierarchical" else 1, world, param])
+        out[f"c{i}_sends"] = np.array([[it.src, it.dst, it.token, it.nbytes]
+                                       for items in sends for it in items], dtype=np.int64)
+        out[f"c{i}_send_rank"] = np.array([r for r, items in enumerate(sends) for _ in items])
+        out[f"c{i}_recv"] = np.array([[r, it.src, it.token] for r, items in enumerate(trace.recv)
+                                      for it in items], dtype=np.int64).reshape(-1, 3)
+        out[f"c{i}_stats"] = np.array([trace.a2a_rounds, trace.allgather_rounds,
+                                       trace.volume_bytes, trace.a2a_volume_bytes,
+                                       trace.reference_bytes], dtype=np.int64)
+    out["n"] = np.array(len(cases))
+    _save("commsim.npz", **out)
+
+
 if __name__ == "__main__":
+    commsim_cases()
     layer_grads()
     route_bench()
     gate_kats()

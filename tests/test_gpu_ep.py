@@ -26,3 +26,6 @@ def test_ep_matches_single_gpu():
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-5000:]
     assert res.stdout.count("transport=nccl") == 5
     assert res.stdout.count("transport=p2p") == 2
+    if n % 2 == 0:
+        assert res.stdout.count("schedule=hierarchical") == 3
+    assert res.stdout.count("schedule=coordinated") >= 3
