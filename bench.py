@@ -60,6 +60,12 @@ def parse():
     ap.add_argument("--decode-iters", type=int, default=50)
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--no-decode-graph", dest="decode_graph", action="store_false")
+    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="N>1 exchange transport (auto: peer memory for k=1 layers)")
+    ap.add_argument("--schedule", default="flat", choices=["flat", "hierarchical"],
+                    help="N>1 nccl all-to-all schedule (commsim.py:239-370)")
+    ap.add_argument("--gpus-per-node", type=int, default=None,
+                    help="node size for --schedule hierarchical (default N/2)")
     return ap.parse_args()
 
 
@@ -226,7 +232,10 @@ def run_gpu(args):
     if world > 1:
         from paper_2201_05596_b200.ep import EPMoeLayer
 
-        layer = EPMoeLayer.synthetic(S, M, E, k, cf, dev, seed=0, residual=residual)
+        gpn = args.gpus_per_node or max(world // 2, 1)
+        layer = EPMoeLayer.synthetic(S, M, E, k, cf, dev, seed=0, residual=residual,
+                                     transport=args.transport, schedule=args.schedule,
+                                     gpus_per_node=gpn if args.schedule == "hierarchical" else None)
     else:
         layer = make_layer(S, M, E, k, cf, dev, residual=residual)
     gen = torch.Generator(device=dev).manual_seed(1 + rank)
@@ -270,7 +279,8 @@ def run_gpu(args):
             s_loc = sd // world
             xd = torch.randn(s_loc, M, device=dev, generator=gen).to(torch.bfloat16)
             # decode runs the layer as one CUDA graph (launch-bound sizes)
-            fwd = layer.graphed(s_loc) if args.decode_graph else layer
+            graph_ok = world == 1 or getattr(layer, "transport", "") == "p2p"
+            fwd = layer.graphed(s_loc) if (args.decode_graph and graph_ok) else layer
             for _ in range(3):
                 fwd(xd)
             lat = []
@@ -366,7 +376,10 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": wl["desc"], "tokens_per_gpu": S, "global_batch": S * world,
-                   "parallelism": f"ep{world}" if world > 1 else "single", "l2": "inputs larger "
+                   "parallelism": f"ep{world}" if world > 1 else "single",
+                   **({"transport": layer.transport, "schedule": layer.schedule}
+                      if world > 1 else {}),
+                   "l2": "inputs larger "
                    "than L2 (x 268 MB, expert weights 8.6 GB per layer)"},
         "roofline": {"bound": "tensor",
                      "kernel": "grouped expert GEMM (GEMM1+GEMM2" +

@@ -202,7 +202,7 @@ class EPMoeLayer:
 
     @classmethod
     def synthetic(cls, S: int, M: int, E: int, k: int, cf: float, dev, seed: int = 0, group=None,
-                  residual: bool = False):
+                  residual: bool = False, **kw):
         """Random-init layer of the named shape (N(0,1)*0.1 weights, zero biases,
         arch.py:347-365), generated on device per expert so every rank draws
         the same gate and its own expert block."""
@@ -228,7 +228,7 @@ class EPMoeLayer:
             shared = FfnParams(torch.randn(M, F, device=dev, generator=gs, dtype=torch.bfloat16) * 0.1,
                                zb1, torch.randn(F, M, device=dev, generator=gs,
                                                 dtype=torch.bfloat16) * 0.1, zb2)
-        return cls(spec, gate_w, experts, shared, group=group, device=dev)
+        return cls(spec, gate_w, experts, shared, group=group, device=dev, **kw)
 
     # ------------------------------------------------------------------
     def _workspace(self, S: int) -> dict:
