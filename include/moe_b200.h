@@ -157,7 +157,12 @@ int moe_load_balance_loss_from_stats(const int32_t* counts, const float* probsum
  * A bf16 (a_rows, K); B bf16 (b_rows, K) with weight w at rows [w*N, w*N+N)
  * (i.e. W^T, K-major); bias f32 (nweights, N) nullable; D bf16 (a_rows, N).
  * rows == NULL means every group has rows_const rows. max_group_rows bounds
- * rows[g] (sizes the launch). act: MOE_ACT_NONE | MOE_ACT_GELU (tanh form). */
+ * rows[g] (sizes the launch). act: MOE_ACT_NONE | MOE_ACT_GELU (tanh form),
+ * optionally | MOE_GEMM_PAD_SCRATCH: the rows [rows[g], row_stride) of each
+ * group's D block are scratch the kernel may overwrite (row_start == NULL), so
+ * whole 32-row boxes go out through TMA tensor stores (the expert buffers'
+ * padding rows; without the flag D rows past rows[g] are never written). */
+#define MOE_GEMM_PAD_SCRATCH 0x100
 int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
                           int N, const float* bias, void* D, int num_groups,
                           const int32_t* row_start, int64_t row_stride, const int32_t* rows,

@@ -14,11 +14,13 @@ import threading
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmoe_b200.so")
+# MOE_B200_LIB: an alternative in-tree build (A/B tuning of compile-time variants)
+LIB_PATH = os.environ.get("MOE_B200_LIB") or os.path.join(HERE, "libmoe_b200.so")
 
 MOE_F32, MOE_BF16, MOE_F64 = 0, 1, 2
 MOE_ACT_NONE, MOE_ACT_GELU = 0, 1
 MOE_ACT_GELU_SAVE, MOE_ACT_GELU_BWD = 3, 4
+MOE_GEMM_PAD_SCRATCH = 0x100  # act flag: rows past each group's count are scratch
 ROUTE_TILE = 128
 MOE_EINVAL = -22
 

@@ -171,9 +171,9 @@ class DenseFfn:
         h = torch.empty((s, self.F), dtype=self.dtype, device=x.device) if h is None else h
         out = torch.empty((s, self.M), dtype=self.dtype, device=x.device) if out is None else out
         _grouped_gemm(self.dtype, x, s, self.M, self.w1, self.F, self.b1, h, 1, None, 0, None, s,
-                      s, _lib.MOE_ACT_GELU)
+                      s, _lib.MOE_ACT_GELU, scratch_pad=True)
         _grouped_gemm(self.dtype, h, s, self.F, self.w2, self.M, self.b2, out, 1, None, 0, None, s,
-                      s, _lib.MOE_ACT_NONE)
+                      s, _lib.MOE_ACT_NONE, scratch_pad=True)
         return out
 
 
@@ -192,9 +192,13 @@ class _Phases:
 
 
 def _grouped_gemm(dtype, a, a_rows, K, w, N, bias, d, G, row_start, row_stride, rows, rows_const,
-                  max_rows, act):
+                  max_rows, act, scratch_pad=False):
+    """scratch_pad: rows past each group's count (up to row_stride) are padding
+    the kernel may overwrite, which lets the bf16 epilogue use TMA tensor stores."""
     st = _lib.stream_ptr()
     if dtype == torch.bfloat16:
+        if scratch_pad:
+            act |= _lib.MOE_GEMM_PAD_SCRATCH
         _lib.call("moe_grouped_gemm_bf16", a.data_ptr(), a_rows, K, w.data_ptr(),
                   w.numel() // K, N, _lib.ptr(bias), d.data_ptr(), G, _lib.ptr(row_start),
                   row_stride, _lib.ptr(rows), rows_const, None, max_rows, act, st)
@@ -390,7 +394,7 @@ class MoeLayer:
             if cap > 0:
                 ph("gemm1")
                 _grouped_gemm(self.dtype, ws["xbuf"], E * cap, M, self.w1, F, self.b1, ws["h"], E,
-                              None, cap, ws["load"], 0, cap, _lib.MOE_ACT_GELU)
+                              None, cap, ws["load"], 0, cap, _lib.MOE_ACT_GELU, scratch_pad=True)
                 ph("gemm2")  # + combine + residual in the epilogue
                 _lib.call("moe_grouped_gemm_bf16_combine", ws["h"].data_ptr(), E * cap, F,
                           self.w2.data_ptr(), E * M, M, self.b2.data_ptr(), E, None, cap,
@@ -404,10 +408,10 @@ class MoeLayer:
         if cap > 0:
             ph("gemm1")
             _grouped_gemm(self.dtype, ws["xbuf"], E * cap, M, self.w1, F, self.b1, ws["h"], E,
-                          None, cap, ws["load"], 0, cap, _lib.MOE_ACT_GELU)
+                          None, cap, ws["load"], 0, cap, _lib.MOE_ACT_GELU, scratch_pad=True)
             ph("gemm2")
             _grouped_gemm(self.dtype, ws["h"], E * cap, F, self.w2, M, self.b2, ws["y"], E, None,
-                          cap, ws["load"], 0, cap, _lib.MOE_ACT_NONE)
+                          cap, ws["load"], 0, cap, _lib.MOE_ACT_NONE, scratch_pad=True)
         shared_out = None
         if self.shared is not None:
             ph("shared_mlp")

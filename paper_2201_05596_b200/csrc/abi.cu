@@ -215,13 +215,16 @@ int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, i
                           int64_t rows_const, const int32_t* weight_idx, int64_t max_group_rows,
                           int act, void* stream) {
   CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1);
+  const int pad_scratch = (act & MOE_GEMM_PAD_SCRATCH) ? 1 : 0;
+  act &= ~MOE_GEMM_PAD_SCRATCH;
   CHECK(act == MOE_ACT_NONE || act == MOE_ACT_GELU);
   CHECK(max_group_rows >= 0 && rows_const >= 0);
   if (a_rows == 0 || max_group_rows == 0) return MOE_OK;
   CHECK(A && B && D);
   return moe::launch_grouped_gemm_bf16(A, a_rows, K, B, b_rows, N, bias, D, num_groups, row_start,
                                        row_stride, rows, rows_const, weight_idx, max_group_rows,
-                                       act, S_(stream));
+                                       act, S_(stream), nullptr, nullptr, nullptr, nullptr, 0,
+                                       pad_scratch);
 }
 
 int moe_grouped_gemm_bf16_combine(const void* A, int64_t a_rows, int K, const void* B,

@@ -84,6 +84,7 @@ struct GemmArgs {
   int64_t k_rows_const;
   int64_t k_stride;
   float* Dacc;                // EPI_WGRAD_ACC output [P, N] fp32
+  int tma_store;    // EPI_BIAS / EPI_BIAS_GELU: whole-box TMA stores through map_d
   int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
   int raster;       // tile order (see tile_at)
   int prefetch;     // L2 prefetch of the next tile's streamed operand
@@ -117,9 +118,15 @@ constexpr uint32_t tmem_cols() {
 // weight-gradient tiles have a short K (one expert's tokens), so the output
 // stream is 4x denser per flop than the forward GEMMs and uncoalesced
 // row-per-thread stores became the bottleneck.
-template <int EPI, int EW>
+// The forward expert GEMMs (EPI_BIAS / EPI_BIAS_GELU, 2-CTA) use the same
+// staging when the caller marks the groups' padding rows as scratch
+// (args.tma_store): bulk tensor stores instead of row-per-lane 16-B stores cut
+// the L2 write transactions of the 1 GB GEMM1 output (energy: the kernel runs
+// at the 1 kW cap).
+template <int EPI, int EW, int CG>
 constexpr int out_stage_bytes() {
-  return EPI == EPI_WGRAD ? EW * 2 * 2048 : 0;
+  return (EPI == EPI_WGRAD || (CG == 2 && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU)))
+             ? EW * 2 * 2048 : 0;
 }
 
 template <int BN, int STAGES, int EPI, int CG, int EW>
@@ -127,7 +134,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_d, GemmArgs args) {
-  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW>()>;
+  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG>()>;
   constexpr int TM = BM * CG;  // rows per tile
   constexpr bool kMN = EPI == EPI_WGRAD || EPI == EPI_WGRAD_ACC;  // MN-major operands
   extern __shared__ uint8_t smem_raw[];
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
-    if constexpr (EPI == EPI_WGRAD) tma_prefetch(&map_d);
+    if (EPI == EPI_WGRAD || args.tma_store) tma_prefetch(&map_d);
   }
   tc_fence_before();
   if constexpr (CG == 2)
@@ -498,35 +505,42 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           }
           tmem_ld_wait_regs(r[c & 1]);
           if (c + 1 < kChunks) tmem_ld_32x32b_x32(t_addr + (c + 1) * 32, r[(c + 1) & 1]);
-          if constexpr (EPI == EPI_WGRAD) {
-            // whole warp: 32 rows x 32 columns -> smem (row = lane, 64 B) -> TMA store;
-            // rows past P / columns past N are clipped by the 3-D map (N, P, G)
-            if (col0 < N) {
-              uint8_t* ob = smem + L::kOutOff + ((warp - 2) * 2 + (ostage & 1)) * 2048;
-              if (lane == 0) bulk_wait_group_read<1>();  // this buffer's previous store has read it
-              __syncwarp();
+          // whole warp: 32 rows x 32 columns -> smem (row = lane, 64 B, 64-B swizzle)
+          // -> one TMA tensor store; rows / columns past the group's block are
+          // clipped by the 3-D map (N, rows per group, G)
+          auto stage_store = [&](const uint32_t (&pk32)[16]) {
+            uint8_t* ob = smem + L::kOutOff + ((warp - 2) * 2 + (ostage & 1)) * 2048;
+            if (lane == 0) bulk_wait_group_read<1>();  // this buffer's previous store has read it
+            __syncwarp();
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint4 pk;
-                const uint32_t* rr = r[c & 1] + 8 * q;
-                pk.x = kzero ? 0u : pack_bf16x2(__uint_as_float(rr[0]), __uint_as_float(rr[1]));
-                pk.y = kzero ? 0u : pack_bf16x2(__uint_as_float(rr[2]), __uint_as_float(rr[3]));
-                pk.z = kzero ? 0u : pack_bf16x2(__uint_as_float(rr[4]), __uint_as_float(rr[5]));
-                pk.w = kzero ? 0u : pack_bf16x2(__uint_as_float(rr[6]), __uint_as_float(rr[7]));
-                const int chunk = q ^ ((lane >> 1) & 3);  // SWIZZLE_64B
-                *reinterpret_cast<uint4*>(ob + lane * 64 + chunk * 16) = pk;
-              }
-              fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                tma_store_3d(&map_d, ob, col0, (int)(mb * TM + cta * BM + quarter * 32), g);
-                bulk_commit_group();
-              }
-              ++ostage;
+            for (int q = 0; q < 4; ++q) {
+              const int chunk = q ^ ((lane >> 1) & 3);  // SWIZZLE_64B
+              *reinterpret_cast<uint4*>(ob + lane * 64 + chunk * 16) =
+                  make_uint4(pk32[4 * q], pk32[4 * q + 1], pk32[4 * q + 2], pk32[4 * q + 3]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&map_d, ob, col0, (int)(mb * TM + cta * BM + quarter * 32), g);
+              bulk_commit_group();
+            }
+            ++ostage;
+          };
+          if constexpr (EPI == EPI_WGRAD) {
+            if (col0 < N) {
+              uint32_t pk32[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                pk32[i] = kzero ? 0u
+                                : pack_bf16x2(__uint_as_float(r[c & 1][2 * i]),
+                                              __uint_as_float(r[c & 1][2 * i + 1]));
+              stage_store(pk32);
             }
             continue;
           }
-          if (!valid || col0 >= N) continue;
+          constexpr bool kTmaEpi = out_stage_bytes<EPI, EW, CG>() > 0 && EPI != EPI_WGRAD;
+          if (col0 >= N) continue;
+          if (!valid && !(kTmaEpi && args.tma_store)) continue;
           float v[32];
           const float4* b4 = reinterpret_cast<const float4*>(sbias + cl);
 #pragma unroll
@@ -602,6 +616,15 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
 #pragma unroll
               for (int i = 0; i < 32; ++i)
                 if (col0 + i < N) v[i] = fmaf(prob, v[i], __bfloat162float(xrow[col0 + i]));
+            }
+          }
+          if constexpr (kTmaEpi) {
+            if (args.tma_store) {
+              uint32_t pk32[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk32[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+              stage_store(pk32);
+              continue;
             }
           }
           if (vec_ok && col0 + 32 <= N) {
@@ -772,7 +795,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         acc_phase ^= 1;
       }
     }
-    if constexpr (EPI == EPI_WGRAD) {
+    if (EPI == EPI_WGRAD || args.tma_store) {
       if (lane == 0) bulk_wait_group_all();
       __syncwarp();
     }
@@ -910,7 +933,7 @@ static int num_sms() {
 template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
                      int64_t max_tiles, cudaStream_t st, const CUtensorMap* md = nullptr) {
-  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW>()>;
+  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG>()>;
   auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -942,7 +965,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              int64_t row_stride, const int32_t* rows, int64_t rows_const,
                              const int32_t* weight_idx, int64_t max_group_rows, int act,
                              cudaStream_t st, const int32_t* row_token, const float* row_prob,
-                             const void* x_resid, void* out, int x_by_row) {
+                             const void* x_resid, void* out, int x_by_row, int pad_scratch) {
   if (G < 1 || G > kMaxGroups || K < 1 || N < 1 || (K % 8) != 0) return MOE_EINVAL;
   int BN = 256;
   if (N <= 32) BN = 32;
@@ -1026,9 +1049,29 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   if (CG == 2 && variant == 1)
     return gelu ? launch_tc<256, 6, EPI_BIAS_GELU, 2, 4>(ma, mb, a, max_tiles, st)
                 : launch_tc<256, 6, EPI_BIAS, 2, 4>(ma, mb, a, max_tiles, st);
-  if (CG == 2)
-    return gelu ? launch_tc<256, 6, EPI_BIAS_GELU, 2, 8>(ma, mb, a, max_tiles, st)
-                : launch_tc<256, 6, EPI_BIAS, 2, 8>(ma, mb, a, max_tiles, st);
+  if (CG == 2) {
+    // whole-box TMA stores when the groups' padding rows are scratch (strided groups)
+    CUtensorMap md;
+    const int64_t per_group = row_stride > 0 ? row_stride : (G == 1 ? rows_const : 0);
+    static const int tma_epi = [] {
+      const char* v = getenv("MOE_TMA_EPILOGUE");
+      return v ? atoi(v) : 1;
+    }();
+#ifndef MOE_FWD_STAGES
+#define MOE_FWD_STAGES 5
+#endif
+#ifndef MOE_FWD_EW
+#define MOE_FWD_EW 8
+#endif
+    if (tma_epi && pad_scratch && row_start == nullptr && per_group > 0 && (N % 8) == 0 &&
+        make_map_out3d(&md, D, G, per_group, N) == 0) {
+      a.tma_store = 1;
+      return gelu ? launch_tc<256, MOE_FWD_STAGES, EPI_BIAS_GELU, 2, MOE_FWD_EW>(ma, mb, a, max_tiles, st, &md)
+                  : launch_tc<256, MOE_FWD_STAGES, EPI_BIAS, 2, MOE_FWD_EW>(ma, mb, a, max_tiles, st, &md);
+    }
+    return gelu ? launch_tc<256, 5, EPI_BIAS_GELU, 2, 8>(ma, mb, a, max_tiles, st)
+                : launch_tc<256, 5, EPI_BIAS, 2, 8>(ma, mb, a, max_tiles, st);
+  }
 #define MOE_TC(BN_, ST_)                                                            \
   return gelu ? launch_tc<BN_, ST_, EPI_BIAS_GELU, 1, (BN_ >= 64 ? 8 : 4)>(ma, mb, a, max_tiles, st) \
               : launch_tc<BN_, ST_, EPI_BIAS, 1, (BN_ >= 64 ? 8 : 4)>(ma, mb, a, max_tiles, st)

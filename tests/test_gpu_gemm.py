@@ -28,9 +28,10 @@ def _ref(a, w_t, bias, rows, starts, widx, act, N):
     return out
 
 
+@pytest.mark.parametrize("pad", [False, True])
 @pytest.mark.parametrize("K,N,act", [(1024, 4096, 1), (4096, 1024, 0), (2048, 8192, 1),
                                      (64, 256, 0), (16, 64, 1), (136, 200, 0), (2048, 96, 1)])
-def test_grouped_gemm_bf16(K, N, act):
+def test_grouped_gemm_bf16(K, N, act, pad):
     torch.manual_seed(K + N)
     G, cap = 5, 300
     rows = [300, 0, 129, 1, 257]
@@ -41,8 +42,8 @@ def test_grouped_gemm_bf16(K, N, act):
     d = torch.full((G * cap, N), float("nan"), device="cuda", dtype=torch.bfloat16)
     rows_t = torch.tensor(rows, dtype=torch.int32, device="cuda")
     _lib.call("moe_grouped_gemm_bf16", a.data_ptr(), G * cap, K, w_t.data_ptr(), G * N, N,
-              bias.data_ptr(), d.data_ptr(), G, None, cap, rows_t.data_ptr(), 0, None, cap, act,
-              _lib.stream_ptr())
+              bias.data_ptr(), d.data_ptr(), G, None, cap, rows_t.data_ptr(), 0, None, cap,
+              act | (_lib.MOE_GEMM_PAD_SCRATCH if pad else 0), _lib.stream_ptr())
     torch.cuda.synchronize()
     ref = _ref(a, w_t, bias, rows, starts, list(range(G)), act, N)
     for g, want in ref.items():
@@ -50,9 +51,9 @@ def test_grouped_gemm_bf16(K, N, act):
         scale = want.abs().mean().item() + 1e-6
         err = (got - want).abs().max().item()
         assert err <= 2e-2 * (want.abs().max().item() + scale), (g, err)
-    # rows beyond each group's count are untouched
-    assert torch.isnan(d[cap:2 * cap].float()).all()
-    assert torch.isnan(d[2 * cap + 129:3 * cap].float()).all()
+    if not pad:  # rows beyond each group's count are untouched
+        assert torch.isnan(d[cap:2 * cap].float()).all()
+        assert torch.isnan(d[2 * cap + 129:3 * cap].float()).all()
 
 
 def test_grouped_gemm_bf16_weight_index_and_row_start():
