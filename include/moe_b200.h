@@ -97,7 +97,8 @@ int moe_dispatch(const void* x, int64_t S, int64_t row_bytes, int E, int k, int6
 
 /* moe_dispatch plus, for the fused-combine path (k=1): row_token / row_prob
  * (E*cap, the token and gate probability behind each expert-buffer row) and,
- * when out_dropped is given, out_dropped[t] = x[t] for fully dropped tokens. */
+ * when out_dropped is given, out_dropped[t] = x[t] for fully dropped tokens.
+ * buf may be NULL (route only: no row copies; see moe_grouped_gemm_bf16_gather). */
 int moe_dispatch_fused(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
                        const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
                        const float* gate_probs, int32_t* slots, void* buf, int32_t* row_token,
@@ -168,6 +169,18 @@ int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, i
                           const int32_t* row_start, int64_t row_stride, const int32_t* rows,
                           int64_t rows_const, const int32_t* weight_idx, int64_t max_group_rows,
                           int act, void* stream);
+
+/* Grouped GEMM with A rows gathered by index (TMA tile::gather4): A row
+ * (g*row_stride + r) = X[row_index[g*row_stride + r]] for r < rows[g]; D, bias,
+ * B, act (incl. MOE_GEMM_PAD_SCRATCH) as moe_grouped_gemm_bf16 with row_start
+ * NULL. The k=1 layer passes x and the row_token table of
+ * moe_dispatch_fused(buf = NULL): the dispatch copy of scatter_tokens
+ * (gating.py:255-278) is done by GEMM1's loads. */
+int moe_grouped_gemm_bf16_gather(const void* X, int64_t x_rows, const int32_t* row_index, int K,
+                                 const void* B, int64_t b_rows, int N, const float* bias, void* D,
+                                 int num_groups, int64_t row_stride, const int32_t* rows,
+                                 int64_t rows_const, int64_t max_group_rows, int act,
+                                 void* stream);
 
 /* GEMM2 of a k=1 layer with combine_tokens and the residual add fused into the
  * epilogue (gating.py:281-307, arch.py:389): for every expert-buffer row r

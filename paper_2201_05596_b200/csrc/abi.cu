@@ -129,8 +129,9 @@ int moe_dispatch_fused(const void* x, int64_t S, int64_t row_bytes, int E, int k
   CHECK(S >= 0 && row_bytes >= 0 && row_bytes % 2 == 0 && E >= 1 && (k == 1 || k == 2) &&
         cap >= 0);
   if (S == 0) return MOE_OK;
-  CHECK(x && ids && local_rank && tile_offsets && gate_probs && slots && row_token && row_prob &&
-        (buf || cap == 0));
+  // buf == NULL: route only (slots, row_token/row_prob, out = x for dropped tokens);
+  // the GEMM then gathers the rows from x (moe_grouped_gemm_bf16_gather)
+  CHECK(x && ids && local_rank && tile_offsets && gate_probs && slots && row_token && row_prob);
   moe::ScatterArgs a;
   a.x = static_cast<const uint8_t*>(x);
   a.S = S, a.row_bytes = row_bytes, a.k = k, a.E = E, a.cap = cap;
@@ -225,6 +226,25 @@ int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, i
                                        row_stride, rows, rows_const, weight_idx, max_group_rows,
                                        act, S_(stream), nullptr, nullptr, nullptr, nullptr, 0,
                                        pad_scratch);
+}
+
+int moe_grouped_gemm_bf16_gather(const void* X, int64_t x_rows, const int32_t* row_index, int K,
+                                 const void* B, int64_t b_rows, int N, const float* bias, void* D,
+                                 int num_groups, int64_t row_stride, const int32_t* rows,
+                                 int64_t rows_const, int64_t max_group_rows, int act,
+                                 void* stream) {
+  CHECK(x_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1 &&
+        row_stride >= 1);
+  const int pad_scratch = (act & MOE_GEMM_PAD_SCRATCH) ? 1 : 0;
+  act &= ~MOE_GEMM_PAD_SCRATCH;
+  CHECK(act == MOE_ACT_NONE || act == MOE_ACT_GELU);
+  CHECK(max_group_rows >= 0 && max_group_rows <= row_stride && rows_const >= 0);
+  if (x_rows == 0 || max_group_rows == 0) return MOE_OK;
+  CHECK(X && row_index && B && D);
+  return moe::launch_grouped_gemm_bf16(X, x_rows, K, B, b_rows, N, bias, D, num_groups, nullptr,
+                                       row_stride, rows, rows_const, nullptr, max_group_rows, act,
+                                       S_(stream), nullptr, nullptr, nullptr, nullptr, 0,
+                                       pad_scratch, row_index);
 }
 
 int moe_grouped_gemm_bf16_combine(const void* A, int64_t a_rows, int K, const void* B,

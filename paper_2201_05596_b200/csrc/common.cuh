@@ -212,6 +212,30 @@ MOE_DEV uint64_t make_sdesc_sw128_mn(const void* smem_ptr) {
   return d;
 }
 
+// TMA row gather: 4 rows (r0..r3) x one 128-B box column into 4 consecutive
+// smem lines (the 128B swizzle follows the smem address, so 32 of these build
+// the same layout as one 128-row tile load). The map's box is {64, 1}.
+MOE_DEV void tma_gather4(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                         int32_t r0, int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3)
+      : "memory");
+}
+// 2-CTA variant: completion signalled on the leader CTA's barrier
+MOE_DEV void tma_gather4_cg2(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                             int32_t r0, int32_t r1, int32_t r2, int32_t r3) {
+  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2),
+      "r"(r3)
+      : "memory");
+}
+
 // TMA tensor store smem -> global (3-D box), tracked by bulk async-groups
 MOE_DEV void tma_store_3d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1,
                           int32_t c2) {

@@ -84,6 +84,10 @@ struct GemmArgs {
   int64_t k_rows_const;
   int64_t k_stride;
   float* Dacc;                // EPI_WGRAD_ACC output [P, N] fp32
+  // A rows gathered by index: A row (g*row_stride + r) = X[a_gather[g*row_stride + r]]
+  // through TMA tile::gather4 (map_a is then a {64, 1}-box map over X): the dispatch
+  // copy of the k=1 layer is folded into GEMM1's producer
+  const int32_t* a_gather;
   int tma_store;    // EPI_BIAS / EPI_BIAS_GELU: whole-box TMA stores through map_d
   int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
   int raster;       // tile order (see tile_at)
@@ -94,6 +98,14 @@ struct GemmArgs {
 // CG = 2: a 2-CTA cluster computes a (2*BM) x BN tile with cta_group::2 (M=256):
 // each CTA loads its own 128 rows of A and BN/2 rows of B, the leader CTA issues
 // the MMAs for the pair, each CTA's TMEM holds its 128 accumulator rows.
+// Accumulator stages in TMEM (512 fp32 columns per lane): two (epilogue of
+// tile i overlaps the MMAs of tile i+1) up to BN = 256; a BN = 512 tile (2-CTA
+// 256 x 512, two N=256 MMAs per K step) fills TMEM, so it has one.
+template <int BN>
+constexpr int acc_stages() {
+  return 2 * BN <= 512 ? 2 : 1;
+}
+
 template <int BN, int STAGES, int CG, int OUT = 0>
 struct Smem {
   static constexpr int kABytes = BM * BK * 2;
@@ -102,15 +114,15 @@ struct Smem {
   static constexpr int kBarOff = STAGES * kStageBytes;
   static constexpr int kBarBytes = (3 * STAGES + 4) * 8 + 16;
   static constexpr int kTileOff = kBarOff + kBarBytes;
-  static constexpr int kBiasOff = (kTileOff + (kMaxGroups + 1) * 4 + 127) / 128 * 128;  // 2 x BN fp32
-  // epilogue staging for TMA stores (weight gradients): OUT bytes, 1024-aligned
-  static constexpr int kOutOff = (kBiasOff + 2 * BN * 4 + 1023) / 1024 * 1024;
+  static constexpr int kBiasOff = (kTileOff + (kMaxGroups + 1) * 4 + 127) / 128 * 128;  // AS x BN fp32
+  // epilogue staging for TMA stores: OUT bytes, 1024-aligned
+  static constexpr int kOutOff = (kBiasOff + acc_stages<BN>() * BN * 4 + 1023) / 1024 * 1024;
   static constexpr int kTotal = kOutOff + OUT + 1024;                    // +1024 align slack
 };
 
 template <int BN>
 constexpr uint32_t tmem_cols() {
-  return (2 * BN) < 32 ? 32 : (2 * BN);
+  return (acc_stages<BN>() * BN) < 32 ? 32 : (acc_stages<BN>() * BN);
 }
 
 // EPI_WGRAD stages each warp's 32 x 32 output chunk in smem (2 x 2 KB per warp,
@@ -123,10 +135,16 @@ constexpr uint32_t tmem_cols() {
 // (args.tma_store): bulk tensor stores instead of row-per-lane 16-B stores cut
 // the L2 write transactions of the 1 GB GEMM1 output (energy: the kernel runs
 // at the 1 kW cap).
-template <int EPI, int EW, int CG>
+// Staging buffers per epilogue warp: 2 (double-buffered) or 1 for BN = 512,
+// whose 48 KB stages leave less room.
+template <int BN>
+constexpr int out_bufs() {
+  return BN > 256 ? 1 : 2;
+}
+template <int EPI, int EW, int CG, int BN = 256>
 constexpr int out_stage_bytes() {
   return (EPI == EPI_WGRAD || (CG == 2 && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU)))
-             ? EW * 2 * 2048 : 0;
+             ? EW * out_bufs<BN>() * 2048 : 0;
 }
 
 template <int BN, int STAGES, int EPI, int CG, int EW>
@@ -134,8 +152,13 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_d, GemmArgs args) {
-  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG>()>;
+  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>()>;
   constexpr int TM = BM * CG;  // rows per tile
+  constexpr int AS = acc_stages<BN>();
+  // MMAs per K step: N <= 256 per tcgen05.mma; a BN = 512 pair tile issues two,
+  // each CTA holding 128 B rows of each (two 16 KB halves of its B stage)
+  constexpr int kNI = (CG == 2 && BN > 256) ? BN / 256 : 1;
+  static_assert(kNI == 1 || (CG == 2 && BN == 512), "BN = 512 needs the 2-CTA pair");
   constexpr bool kMN = EPI == EPI_WGRAD || EPI == EPI_WGRAD_ACC;  // MN-major operands
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -186,7 +209,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         mbar_init(&full[s], CG);  // CG=2: the peer's producer arrives remotely on the leader's
         mbar_init(&empty[s], 1);
       }
-      for (int a = 0; a < 2; ++a) {
+      for (int a = 0; a < AS; ++a) {
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], EW * CG);  // every epilogue warp of the pair arrives
       }
@@ -255,6 +278,17 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       const int w = args.weight_idx ? args.weight_idx[g] : g;
       const int a_row = (int)(rs + (int64_t)mb * TM + cta * BM);
       const int b_row = w * args.N + nb * BN + cta * (BN / CG);
+      // gather mode: this lane's 4 source rows of the CTA's 128-row A tile (rows past
+      // the group's count read row 0: their outputs are padding)
+      int grow[4] = {0, 0, 0, 0};
+      if (!kMN && args.a_gather != nullptr) {
+        const int64_t rg = args.rows ? args.rows[g] : args.rows_const;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t lr = (int64_t)mb * TM + cta * BM + 4 * lane + i;
+          grow[i] = lr < rg ? args.a_gather[rs + lr] : 0;
+        }
+      }
       if (args.prefetch && lane == 0) {
         // Warm L2 with the NEXT tile's streamed operand while this one runs: the
         // smem ring alone keeps too few DRAM bytes in flight per SM to hide the
@@ -332,10 +366,48 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           }
           continue;
         }
-        if (lane == 0) {
+        if (args.a_gather != nullptr) {
+          // A: 32 lanes x gather4 (4 rows x 128 B each); B: one tile load
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           if constexpr (CG == 2) {
+            tma_gather4_cg2(sa + 512 * lane, &map_a, &full[stage], kb * BK, grow[0], grow[1],
+                            grow[2], grow[3]);
+            if (lane == 0) {
+              if constexpr (kNI > 1) {
+#pragma unroll
+                for (int i = 0; i < kNI; ++i)
+                  tma_load_2d_cg2(sb + i * 128 * BK * 2, &map_b, &full[stage], kb * BK,
+                                  w * args.N + nb * BN + i * 256 + (int)cta * 128);
+              } else {
+                tma_load_2d_cg2(sb, &map_b, &full[stage], kb * BK, b_row);
+              }
+              if (leader)
+                mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+              else
+                mbar_arrive_cluster(&full[stage], 0);
+            }
+          } else {
+            if (lane == 0) mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+            __syncwarp();
+            tma_gather4(sa + 512 * lane, &map_a, &full[stage], kb * BK, grow[0], grow[1], grow[2],
+                        grow[3]);
+            if (lane == 0) tma_load_2d(sb, &map_b, &full[stage], kb * BK, b_row);
+          }
+        } else if (lane == 0) {
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          if constexpr (kNI > 1) {
+            tma_load_2d_cg2(sa, &map_a, &full[stage], kb * BK, a_row);
+#pragma unroll
+            for (int i = 0; i < kNI; ++i)  // B rows of MMA i: [nb*BN + i*256 + cta*128, +128)
+              tma_load_2d_cg2(sb + i * 128 * BK * 2, &map_b, &full[stage], kb * BK,
+                              w * args.N + nb * BN + i * 256 + (int)cta * 128);
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+            else
+              mbar_arrive_cluster(&full[stage], 0);
+          } else if constexpr (CG == 2) {
             tma_load_2d_cg2(sa, &map_a, &full[stage], kb * BK, a_row);
             tma_load_2d_cg2(sb, &map_b, &full[stage], kb * BK, b_row);
             if (leader)
@@ -357,7 +429,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only; lane 0 issues, whole warp waits)
-    constexpr uint32_t idesc = kMN ? make_idesc_bf16_mn(TM, BN) : make_idesc_bf16(TM, BN);
+    constexpr uint32_t idesc = kMN ? make_idesc_bf16_mn(TM, BN) : make_idesc_bf16(TM, BN / kNI);
     // K step of one MMA (16 elements): +32 B inside the swizzle line (K-major) or
     // two 8-row groups (+2048 B, MN-major); descriptor units are 16 B
     constexpr uint64_t kStep = kMN ? 128 : 2;
@@ -388,10 +460,17 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           const uint64_t bdesc = kMN ? make_sdesc_sw128_mn(sb) : make_sdesc_sw128(sb);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            if constexpr (CG == 2)
+            if constexpr (kNI > 1) {
+#pragma unroll
+              for (int i = 0; i < kNI; ++i)  // B half i = 128 rows x 128 B further (>>4: +1024)
+                umma_bf16_cg2(d_tmem + i * 256, adesc + kStep * kk,
+                              bdesc + (uint64_t)i * ((128 * BK * 2) >> 4) + kStep * kk, idesc,
+                              (kb | kk) != 0);
+            } else if constexpr (CG == 2) {
               umma_bf16_cg2(d_tmem, adesc + kStep * kk, bdesc + kStep * kk, idesc, (kb | kk) != 0);
-            else
+            } else {
               umma_bf16(d_tmem, adesc + kStep * kk, bdesc + kStep * kk, idesc, (kb | kk) != 0);
+            }
           }
           if constexpr (CG == 2)
             umma_commit_cg2(&empty[stage], 0x3);  // frees the stage in both CTAs
@@ -411,7 +490,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           umma_commit(&tfull[acc]);
       }
       __syncwarp();
-      if (++acc == 2) {
+      if (++acc == AS) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -509,8 +588,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           // -> one TMA tensor store; rows / columns past the group's block are
           // clipped by the 3-D map (N, rows per group, G)
           auto stage_store = [&](const uint32_t (&pk32)[16]) {
-            uint8_t* ob = smem + L::kOutOff + ((warp - 2) * 2 + (ostage & 1)) * 2048;
-            if (lane == 0) bulk_wait_group_read<1>();  // this buffer's previous store has read it
+            constexpr int OB = out_bufs<BN>();
+            uint8_t* ob = smem + L::kOutOff + ((warp - 2) * OB + (ostage % OB)) * 2048;
+            if (lane == 0) bulk_wait_group_read<OB - 1>();  // this buffer's last store has read it
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -538,7 +618,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             }
             continue;
           }
-          constexpr bool kTmaEpi = out_stage_bytes<EPI, EW, CG>() > 0 && EPI != EPI_WGRAD;
+          constexpr bool kTmaEpi = out_stage_bytes<EPI, EW, CG, BN>() > 0 && EPI != EPI_WGRAD;
           if (col0 >= N) continue;
           if (!valid && !(kTmaEpi && args.tma_store)) continue;
           float v[32];
@@ -790,7 +870,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
                 wc[e] + wc[E + e] + wc[2 * E + e] + wc[3 * E + e];
         named_bar_sync(1, 128);
       }
-      if (++acc == 2) {
+      if (++acc == AS) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -933,7 +1013,7 @@ static int num_sms() {
 template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
                      int64_t max_tiles, cudaStream_t st, const CUtensorMap* md = nullptr) {
-  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG>()>;
+  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>()>;
   auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -965,7 +1045,8 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              int64_t row_stride, const int32_t* rows, int64_t rows_const,
                              const int32_t* weight_idx, int64_t max_group_rows, int act,
                              cudaStream_t st, const int32_t* row_token, const float* row_prob,
-                             const void* x_resid, void* out, int x_by_row, int pad_scratch) {
+                             const void* x_resid, void* out, int x_by_row, int pad_scratch,
+                             const int32_t* a_gather) {
   if (G < 1 || G > kMaxGroups || K < 1 || N < 1 || (K % 8) != 0) return MOE_EINVAL;
   int BN = 256;
   if (N <= 32) BN = 32;
@@ -989,7 +1070,8 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   }();
   const int CG = (BN == 256 && max_group_rows > BM && variant != 2) ? 2 : 1;
   CUtensorMap ma, mb;
-  int rc = make_map(&ma, A, a_rows, K, BM);
+  // gather mode: A is the token matrix X (a_rows rows), one 128-B box row per gather lane
+  int rc = make_map(&ma, A, a_rows, K, a_gather ? 1 : BM);
   if (rc) return rc;
   rc = make_map(&mb, B, b_rows, K, BN / CG);
   if (rc) return rc;
@@ -1009,6 +1091,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.x_resid = (const __nv_bfloat16*)x_resid;
   a.out = (__nv_bfloat16*)out;
   a.x_by_row = x_by_row;
+  a.a_gather = a_gather;
   a.stream_hint = stream_hint;
   a.raster = raster;
   a.prefetch = prefetch_mode() & 2 ? 1 : 0;
@@ -1063,6 +1146,21 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
 #ifndef MOE_FWD_EW
 #define MOE_FWD_EW 8
 #endif
+    static const int bn512 = [] {
+      const char* v = getenv("MOE_BN512");
+      return v ? atoi(v) : 0;
+    }();
+    if (bn512 && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
+        (N % 512) == 0 && make_map_out3d(&md, D, G, per_group, N) == 0) {
+      // 256 x 512 pair tiles: 25% less operand traffic per flop, no accumulator overlap
+      CUtensorMap mb2;
+      rc = make_map(&mb2, B, b_rows, K, 128);
+      if (rc) return rc;
+      a.tma_store = 1;
+      const int64_t tiles512 = (int64_t)G * ((max_group_rows + tm - 1) / tm) * ((N + 511) / 512);
+      return gelu ? launch_tc<512, 4, EPI_BIAS_GELU, 2, 8>(ma, mb2, a, tiles512, st, &md)
+                  : launch_tc<512, 4, EPI_BIAS, 2, 8>(ma, mb2, a, tiles512, st, &md);
+    }
     if (tma_epi && pad_scratch && row_start == nullptr && per_group > 0 && (N % 8) == 0 &&
         make_map_out3d(&md, D, G, per_group, N) == 0) {
       a.tma_store = 1;

@@ -59,7 +59,8 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              const int32_t* weight_idx, int64_t max_group_rows, int act,
                              cudaStream_t st, const int32_t* row_token = nullptr,
                              const float* row_prob = nullptr, const void* x_resid = nullptr,
-                             void* out = nullptr, int x_by_row = 0, int pad_scratch = 0);
+                             void* out = nullptr, int x_by_row = 0, int pad_scratch = 0,
+                             const int32_t* a_gather = nullptr);
 
 int launch_wgrad_bf16(const void* X, int64_t x_rows, int P, const void* Y, int Q, int G,
                       int64_t k_stride, const int32_t* k_rows, int64_t k_rows_const, void* D,

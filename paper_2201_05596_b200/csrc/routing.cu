@@ -318,9 +318,14 @@ __global__ void scatter_kernel(ScatterArgs a) {
       }
       if (a.row_index != nullptr && lane == 0) a.row_index[t * k + j] = (int32_t)d;
     }
-    V* d0 = dst0 >= 0 ? reinterpret_cast<V*>(base0 + dst0 * a.row_bytes) : nullptr;
-    V* d1 = dst1 >= 0 ? reinterpret_cast<V*>(base1 + dst1 * a.row_bytes) : nullptr;
-    if (d0 == nullptr && d1 == nullptr) {
+    V* d0 = nullptr;
+    V* d1 = nullptr;
+    if (dst0 >= 0 || dst1 >= 0) {
+      // route-only mode (no expert buffer): the grouped GEMM gathers the row itself
+      if (a.buf == nullptr && a.peer_buf == nullptr) continue;
+      d0 = dst0 >= 0 ? reinterpret_cast<V*>(base0 + dst0 * a.row_bytes) : nullptr;
+      d1 = dst1 >= 0 ? reinterpret_cast<V*>(base1 + dst1 * a.row_bytes) : nullptr;
+    } else {
       if (a.out_dropped == nullptr) continue;
       d0 = reinterpret_cast<V*>(a.out_dropped + t * a.row_bytes);  // out = x
     }

@@ -165,3 +165,31 @@ def test_colsum_rows():
     for g, n in enumerate(rows):
         want = x[g * cap:g * cap + n].double().sum(0)
         assert torch.allclose(out[g].double(), want, atol=1e-3, rtol=1e-5), g
+
+
+@pytest.mark.parametrize("K,N,act,cap", [(2048, 8192, 1, 512), (1024, 1024, 0, 300), (256, 96, 1, 40),
+                                         (136, 200, 0, 129), (512, 4096, 1, 3)])
+def test_grouped_gemm_bf16_gather(K, N, act, cap):
+    """A rows gathered by index (TMA gather4): equal to the GEMM on the gathered copy."""
+    torch.manual_seed(K + N + cap)
+    G, S = 5, 700
+    rows = [cap, 0, max(cap // 2, 1), 1, min(cap, 257)]
+    x = (torch.randn(S, K, device="cuda") * 0.5).to(torch.bfloat16)
+    idx = torch.randint(0, S, (G * cap,), dtype=torch.int32, device="cuda")
+    w_t = (torch.randn(G * N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(G, N, device="cuda") * 0.1
+    rows_t = torch.tensor(rows, dtype=torch.int32, device="cuda")
+    d = torch.full((G * cap, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    _lib.call("moe_grouped_gemm_bf16_gather", x.data_ptr(), S, idx.data_ptr(), K, w_t.data_ptr(),
+              G * N, N, bias.data_ptr(), d.data_ptr(), G, cap, rows_t.data_ptr(), 0, cap,
+              act | _lib.MOE_GEMM_PAD_SCRATCH, _lib.stream_ptr())
+    # the same GEMM on the materialised gather
+    a = x[idx.long()]
+    d2 = torch.full_like(d, float("nan"))
+    _lib.call("moe_grouped_gemm_bf16", a.data_ptr(), G * cap, K, w_t.data_ptr(), G * N, N,
+              bias.data_ptr(), d2.data_ptr(), G, None, cap, rows_t.data_ptr(), 0, None, cap,
+              act | _lib.MOE_GEMM_PAD_SCRATCH, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    for g, r in enumerate(rows):
+        got, want = d[g * cap:g * cap + r], d2[g * cap:g * cap + r]
+        assert torch.equal(got, want), (g, (got.float() - want.float()).abs().max().item())

@@ -331,3 +331,19 @@ def test_bf16_limits_raise():
                             np.random.default_rng(0))
     with pytest.raises((ValueError, A.ShapeError)):
         A.MoeLayer(spec, p, dtype=torch.bfloat16)
+
+
+@pytest.mark.parametrize("S,M,E,cf", [(4096, 1024, 16, 1.0), (3000, 512, 8, 0.6), (200, 256, 4, 2.0)])
+def test_gather_rows_matches_dispatched_copy(S, M, E, cf):
+    """k=1 fused path: GEMM1 gathering its rows from x (TMA gather4) is bit-identical
+    to GEMM1 on the dispatched expert buffer."""
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, 1, cf))
+    p = A.init_layer_params(spec, np.random.default_rng(S))
+    x = torch.randn(S, M, device="cuda").to(torch.bfloat16)
+    outs = []
+    for gather in (True, False):
+        layer = A.MoeLayer(spec, p, dtype=torch.bfloat16, gather_rows=gather)
+        assert layer.gather_rows == gather
+        outs.append(layer(x))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
