@@ -269,6 +269,16 @@ MOE_DEV void mbar_arrive_cluster_release(uint64_t* bar, uint32_t cta) {
       : "memory");
 }
 
+// 32-bit store into CTA `cta`'s copy of an smem location (distributed shared memory)
+MOE_DEV void st_shared_cluster_i32(int* p, uint32_t cta, int v) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "st.shared::cluster.b32 [ra], %2;\n\t}" ::"r"(smem_u32(p)),
+      "r"(cta), "r"(v)
+      : "memory");
+}
+
 // fire-and-forget vector fp32 add to global memory (16-byte aligned)
 MOE_DEV void red_add_v4_f32(float* dst, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c),

@@ -50,6 +50,7 @@ constexpr int threads_for() {
   return 64 + 32 * EW + ((EPI == EPI_WGRAD || EPI == EPI_WGRAD_ACC) ? 32 : 0);
 }
 constexpr int kMaxGroups = 2048;
+constexpr int kTileQ = 8;  // dynamic tile scheduler: queue depth (producer runs <= ~3 tiles ahead)
 
 struct GemmArgs {
   const float* bias;          // [num_weights, N] fp32 (may be null)
@@ -84,6 +85,11 @@ struct GemmArgs {
   int64_t k_rows_const;
   int64_t k_stride;
   float* Dacc;                // EPI_WGRAD_ACC output [P, N] fp32
+  // dynamic tile scheduling: tiles are claimed in order with atomicAdd on this
+  // (zeroed) counter by the leader's producer and handed to the pair's warps
+  // through an smem queue, so the clusters that share a weight tile stay in step
+  // (static round robin drifts and re-reads weights from HBM); null = static
+  int* tile_counter;
   // A rows gathered by index: A row (g*row_stride + r) = X[a_gather[g*row_stride + r]]
   // through TMA tile::gather4 (map_a is then a {64, 1}-box map over X): the dispatch
   // copy of the k=1 layer is folded into GEMM1's producer
@@ -112,7 +118,9 @@ struct Smem {
   static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOff = STAGES * kStageBytes;
-  static constexpr int kBarBytes = (3 * STAGES + 4) * 8 + 16;
+  // full/empty ring, 2 x tfull/tempty, tmem slot, pbar ring, tile-queue full/empty
+  // barriers and the tile-queue slots (dynamic scheduling)
+  static constexpr int kBarBytes = (3 * STAGES + 4 + 2 * kTileQ) * 8 + 16 + kTileQ * 4;
   static constexpr int kTileOff = kBarOff + kBarBytes;
   static constexpr int kBiasOff = (kTileOff + (kMaxGroups + 1) * 4 + 127) / 128 * 128;  // AS x BN fp32
   // epilogue staging for TMA stores: OUT bytes, 1024-aligned
@@ -169,6 +177,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint64_t* pbar = tempty + 3;  // [STAGES] weight-gradient partial K blocks (CTA-local)
+  uint64_t* tq_full = pbar + STAGES;   // [kTileQ]
+  uint64_t* tq_empty = tq_full + kTileQ;
+  volatile int* tq = reinterpret_cast<volatile int*>(tq_empty + kTileQ);
   int32_t* tile_start = reinterpret_cast<int32_t*>(smem + L::kTileOff);
 
   const uint32_t warp = warp_id_uniform();
@@ -214,6 +225,13 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         mbar_init(&tempty[a], EW * CG);  // every epilogue warp of the pair arrives
       }
       for (int s = 0; s < STAGES; ++s) mbar_init(&pbar[s], 1);
+      // tile queue: full = the leader producer's (remote) arrive; empty (leader's) = every
+      // consumer warp of the pair: MMA + epilogue (+ fix-up) warps, and the peer's producer
+      constexpr int kFix = kMN ? 1 : 0;
+      for (int q = 0; q < kTileQ; ++q) {
+        mbar_init(&tq_full[q], 1);
+        mbar_init(&tq_empty[q], CG == 2 ? 2 + 2 * EW + 2 * kFix : 1 + EW + kFix);
+      }
       mbar_fence_init();
     }
     __syncwarp();
@@ -243,7 +261,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   // run the other m-blocks of the same n-blocks share each weight tile.
   // args.raster: 0 = plain round robin with m fastest (concurrent clusters share
   // the weight tile), 1 = round robin over runs of 4 n-blocks with n fastest.
-  const int kRun = args.raster == 1 ? 4 : 1;
+  // raster 2: as 0 (m fastest) but each pair takes runs of 2 tiles: both m-blocks
+  // of a (group, n-block) back to back, the weight tile re-read from L2
+  const int kRun = args.raster == 1 ? 4 : (args.raster == 2 ? 2 : 1);
   auto tile_at = [&](int it) {
     return ((it / kRun) * work_stride + work_id) * kRun + (it % kRun);
   };
@@ -262,6 +282,48 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     }
   };
 
+  // next tile for loop iteration `it` (whole warp), -1 when done. Static: round
+  // robin. Dynamic: the leader's producer claims tiles and publishes them to both
+  // CTAs' queues; every other role reads its CTA's queue and frees the slot.
+  const bool dyn = args.tile_counter != nullptr;
+  int claimed = -1;  // writer (lane 0): the tile claimed one iteration ahead
+  auto fetch = [&](int it, bool writer) -> int {
+    if (!dyn) {
+      const int t = tile_at(it);
+      return t < total_tiles ? t : -1;
+    }
+    const int slot = it % kTileQ;
+    const uint32_t ph = (uint32_t)(it / kTileQ) & 1u;
+    int t = 0;
+    if (writer) {
+      mbar_wait(&tq_empty[slot], ph ^ 1u);
+      if (lane == 0) {
+        // claim one tile ahead: the atomic's round trip overlaps this tile's loads
+        if (it == 0) claimed = atomicAdd(args.tile_counter, 1);
+        t = claimed < total_tiles ? claimed : -1;
+        if (t >= 0) claimed = atomicAdd(args.tile_counter, 1);
+        tq[slot] = t;
+        if constexpr (CG == 2) {
+          st_shared_cluster_i32(const_cast<int*>(&tq[slot]), 1, t);
+          mbar_arrive_cluster_release(&tq_full[slot], 1);
+        }
+        mbar_arrive(&tq_full[slot]);
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+    } else {
+      mbar_wait(&tq_full[slot], ph);
+      t = tq[slot];
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2 && !leader)
+          mbar_arrive_cluster_release(&tq_empty[slot], 0);
+        else
+          mbar_arrive(&tq_empty[slot]);
+      }
+    }
+    return t;
+  };
+
   if (warp == 0) {
     // ===================== TMA producer (both CTAs of a pair load their halves)
     int stage = 0;
@@ -271,7 +333,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     // (L2 eviction-priority hints on A/B were measured and removed: evict_first
     // on the weights raised DRAM traffic from 6.2 to 9.1 GB per GEMM1 launch)
     int gp = 0;  // group cursor for the prefetch look-ahead
-    for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
+    for (int it = 0;; ++it) {
+      const int tile = fetch(it, leader);
+      if (tile < 0) break;
       int mb, nb;
       decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
@@ -289,7 +353,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           grow[i] = lr < rg ? args.a_gather[rs + lr] : 0;
         }
       }
-      if (args.prefetch && lane == 0) {
+      if (args.prefetch && !dyn && lane == 0) {
         // Warm L2 with the NEXT tile's streamed operand while this one runs: the
         // smem ring alone keeps too few DRAM bytes in flight per SM to hide the
         // loaded HBM latency (x for the gate, the weights for the expert GEMMs).
@@ -439,7 +503,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     uint32_t acc_phase = 0;
     const int num_kb = (args.K + BK - 1) / BK;
     int g = 0;
-    for (int it = 0, tile = tile_at(0); leader && tile < total_tiles; tile = tile_at(++it)) {
+    for (int it = 0; leader; ++it) {
+      const int tile = fetch(it, false);
+      if (tile < 0) break;
       int kb_end = num_kb;
       if constexpr (kMN) {
         int mb_, nb_;
@@ -516,7 +582,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         named_bar_sync(1, 128);
       }
     }
-    for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
+    for (int it = 0;; ++it) {
+      const int tile = fetch(it, false);
+      if (tile < 0) break;
       int mb, nb;
       decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
@@ -895,7 +963,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     uint32_t pph = 0;  // per-stage parity of pbar
     int g = 0;
     constexpr int kBoxB = (BN / CG) / 64;
-    for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
+    for (int it = 0;; ++it) {
+      const int tile = fetch(it, false);
+      if (tile < 0) break;
       int mb, nb;
       decode(tile, g, mb, nb);
       const int kg = (int)(args.k_rows ? args.k_rows[g] : args.k_rows_const);
@@ -1000,6 +1070,43 @@ static int prefetch_mode() {
   return m;
 }
 
+// Dynamic-scheduling tile counters: a per-device pool, one zeroed (stream-ordered
+// memset) slot per launch, rotating so launches in flight on other streams do not
+// share a counter. MOE_DYN_SCHED=0 restores static round robin.
+// mode 2 (default): only long-K launches (K >= 2N, the GEMM2 shape: few long
+// tiles, where keeping the weight-sharing pairs in step pays: GEMM2 1.65 vs
+// 1.70 ms in the C3 layer); 1: every launch (GEMM1, 4x more and shorter tiles,
+// loses 2-4% to the queue hand-off); 0: static round robin everywhere.
+static int* dyn_counter(cudaStream_t st, int64_t K = 0, int64_t N = 0) {
+  static const int enabled = [] {
+    const char* v = getenv("MOE_DYN_SCHED");
+    return v ? atoi(v) : 2;
+  }();
+  if (!enabled || (enabled == 2 && K < 2 * N)) return nullptr;
+  constexpr int kPool = 4096;
+  static int* pool[64] = {};
+  static unsigned next[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  int* c = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (pool[dev] == nullptr) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs != cudaStreamCaptureStatusNone) return nullptr;  // no allocation inside a capture
+      if (cudaMalloc(&pool[dev], kPool * sizeof(int)) != cudaSuccess) {
+        pool[dev] = nullptr;
+        return nullptr;
+      }
+    }
+    c = pool[dev] + (next[dev]++ % kPool);
+  }
+  if (cudaMemsetAsync(c, 0, sizeof(int), st) != cudaSuccess) return nullptr;
+  return c;
+}
+
 static int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -1022,6 +1129,14 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
     attr_done = true;
   }
   int64_t grid = num_sms();
+  static const int nonpersist = [] {
+    const char* v = getenv("MOE_NONPERSIST");
+    return v ? atoi(v) : 0;
+  }();
+  // non-persistent: one CTA (pair) per tile, the hardware block scheduler hands
+  // out tiles in order as SMs free up (no drift between the pairs that share a
+  // weight tile)
+  if (nonpersist && EPI != EPI_GATE && max_tiles * CG > grid) grid = max_tiles * CG;
   if (max_tiles * CG < grid) grid = max_tiles < 1 ? CG : max_tiles * CG;
   grid -= grid % CG;
   cudaLaunchConfig_t cfg{};
@@ -1092,6 +1207,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.out = (__nv_bfloat16*)out;
   a.x_by_row = x_by_row;
   a.a_gather = a_gather;
+  a.tile_counter = dyn_counter(st, K, N);
   a.stream_hint = stream_hint;
   a.raster = raster;
   a.prefetch = prefetch_mode() & 2 ? 1 : 0;
@@ -1214,6 +1330,7 @@ int launch_wgrad_bf16(const void* X, int64_t x_rows, int P, const void* Y, int Q
   a.k_stride = k_stride;
   a.D = acc ? nullptr : (__nv_bfloat16*)D;
   a.Dacc = acc ? (float*)D : nullptr;
+  a.tile_counter = dyn_counter(st);
   a.stream_hint = acc ? 0 : stream_hint;
   const int64_t tiles = (int64_t)G * ((P + BM * CG - 1) / (BM * CG)) * ((Q + BN - 1) / BN);
   if (x_rows == 0 && acc) return 0;
