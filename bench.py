@@ -50,7 +50,7 @@ WORKLOADS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (default: workload's)")
@@ -104,15 +104,22 @@ def run_reference(args):
         return
     cores = len(os.sched_getaffinity(0))
     times, state = [], None
+    # each step is ~1.3 s of CPU work: the timed steps stop once ~150 s are spent so
+    # the arm ends within a few minutes whatever --steps is (the line reports both)
+    t_start = None
     for i in range(args.warmup + args.steps):
         dt, state = cpu_reference_step(state)
         if i >= args.warmup:
             times.append(dt)
+            t_start = t_start or time.time() - dt
+            if time.time() - t_start > 150.0:
+                break
     med = statistics.median(times)
     value = CPU_SAMPLE["S"] / med
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": len(times), "steps_requested": args.steps,
+        "warmup": args.warmup,
         "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS["c3"]["desc"], "tokens_per_gpu": WORKLOADS["c3"]["S"],
@@ -132,23 +139,34 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi sampler (every 25 ms), started before the warm-up so it is up
+    when the timed region begins; only samples stamped inside [mark(), stop()]
+    are kept."""
+
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
         self.idx = gpu_index
+        self.t0 = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "25"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
 
+    def mark(self) -> None:
+        self.t0 = time.time()
+
     def stop(self) -> dict:
+        import datetime
+
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.time()
         self.p.terminate()
         self.p.wait()
         self.f.flush()
@@ -158,6 +176,9 @@ class Clocks:
             if len(parts) < 9:
                 continue
             try:
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if self.t0 is not None and not (self.t0 <= ts <= t1):
+                    continue
                 rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
             except ValueError:
                 continue
@@ -242,6 +263,7 @@ def run_gpu(args):
     x = torch.randn(S, M, device=dev, generator=gen).to(torch.bfloat16)
     # drop-free synthetic routing at C3 with unbiased logits is ~1.9% drops
     out = torch.empty_like(x)
+    clocks = Clocks(local) if rank == 0 else None
     for _ in range(args.warmup):
         layer(x, out=out)
     torch.cuda.synchronize()
@@ -249,10 +271,11 @@ def run_gpu(args):
     # ---- timed region: K full forwards, inputs resident (x 268 MB + weights 8.6 GB >> L2)
     timer = _lib.PhaseTimer()
     launches0 = _lib.launch_count()
-    clocks = Clocks(local) if rank == 0 else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if clocks:
+        clocks.mark()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
