@@ -64,6 +64,10 @@ def parse():
                     help="N>1 exchange transport (auto: peer memory for k=1 layers)")
     ap.add_argument("--schedule", default="flat", choices=["flat", "hierarchical"],
                     help="N>1 nccl all-to-all schedule (commsim.py:239-370)")
+    ap.add_argument("--chunks", type=int, default=1,
+                    help="N>1 p2p: token chunks pipelined through dispatch / GEMMs / pull")
+    ap.add_argument("--comm-sms", type=int, default=16,
+                    help="SMs the GEMMs leave to the copy kernels when chunked")
     ap.add_argument("--gpus-per-node", type=int, default=None,
                     help="node size for --schedule hierarchical (default N/2)")
     return ap.parse_args()
@@ -256,7 +260,8 @@ def run_gpu(args):
         gpn = args.gpus_per_node or max(world // 2, 1)
         layer = EPMoeLayer.synthetic(S, M, E, k, cf, dev, seed=0, residual=residual,
                                      transport=args.transport, schedule=args.schedule,
-                                     gpus_per_node=gpn if args.schedule == "hierarchical" else None)
+                                     gpus_per_node=gpn if args.schedule == "hierarchical" else None,
+                                     chunks=args.chunks, comm_sms=args.comm_sms)
     else:
         layer = make_layer(S, M, E, k, cf, dev, residual=residual)
     gen = torch.Generator(device=dev).manual_seed(1 + rank)
@@ -400,7 +405,8 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": wl["desc"], "tokens_per_gpu": S, "global_batch": S * world,
                    "parallelism": f"ep{world}" if world > 1 else "single",
-                   **({"transport": layer.transport, "schedule": layer.schedule}
+                   **({"transport": layer.transport, "schedule": layer.schedule,
+                       "chunks": getattr(layer, "chunks", 1)}
                       if world > 1 else {}),
                    "l2": "inputs larger "
                    "than L2 (x 268 MB, expert weights 8.6 GB per layer)"},

@@ -280,6 +280,20 @@ int moe_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap, 
                 int32_t* row_base, int32_t* seg_start, int32_t* seg_rows, int32_t* recv_rows,
                 void* stream);
 
+/* moe_ep_plan for C token chunks per rank (chunk c of rank s = its tokens
+ * [c*S/C, (c+1)*S/C)): counts (world, C, E); outputs per chunk: slot_base
+ * (C, E), row_base (C, E), seg_start / seg_rows (C, E/world), recv_rows (C);
+ * the owners' receive buffers are chunk-major, so chunk c can be exchanged
+ * while chunk c-1 is in the GEMMs. C = 1 is moe_ep_plan. */
+int moe_ep_plan_chunked(const int32_t* counts, int world, int rank, int E, int chunks, int64_t cap,
+                        int32_t* slot_base, int32_t* row_base, int32_t* seg_start,
+                        int32_t* seg_rows, int32_t* recv_rows, void* stream);
+
+/* Launch limits of the calling host thread (0 = none): the persistent GEMMs
+ * use at most gemm_ctas CTAs and the dispatch / pull copy kernels at most
+ * comm_blocks blocks, so an exchange can run beside a GEMM on the SMs left. */
+int moe_set_launch_limits(int gemm_ctas, int comm_blocks);
+
 /* System-scope flag barrier over peer signal pads: epoch = *epoch_counter + 1
  * (a device counter, so the barrier can be captured in a CUDA graph) is
  * written into slot [rank] of every peer's pad (peer_signal: device array of

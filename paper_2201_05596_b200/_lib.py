@@ -73,6 +73,8 @@ SIGNATURES = {
     "moe_combine_bwd_bf16": (_I, [_P, _P, _L, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
     "moe_gate_bwd": (_I, [_P, _L, _I, _I, _I, _P, _P, _P, _P, _I, _P]),
     "moe_gather_rows": (_I, [_P, _L, _P, _L, _P, _P]),
+    "moe_ep_plan_chunked": (_I, [_P, _I, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
+    "moe_set_launch_limits": (_I, [_I, _I]),
     "moe_grouped_gemm_bf16_gather": (_I, [_P, _L, _P, _I, _P, _L, _I, _P, _P, _I, _L, _P, _L, _L,
                                           _I, _P]),
     "moe_colsum_rows_bf16": (_I, [_P, _I, _I, _L, _P, _L, _P, _P]),

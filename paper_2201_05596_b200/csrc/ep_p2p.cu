@@ -21,46 +21,77 @@
 
 namespace moe {
 
+// Launch limits for overlapping an exchange with the GEMMs on one GPU: the GEMM
+// leaves SMs free (persistent grid capped) and the copy kernels stay inside
+// them. Thread-local (set around the launches by the host thread issuing them).
+static thread_local int t_gemm_ctas = 0, t_comm_blocks = 0;
+void set_launch_limits(int gemm_ctas, int comm_blocks) {
+  t_gemm_ctas = gemm_ctas;
+  t_comm_blocks = comm_blocks;
+}
+int gemm_cta_limit() { return t_gemm_ctas; }
+int comm_block_limit() { return t_comm_blocks; }
+
+// Exchange plan from the all-gathered per-(rank, chunk, expert) counts, C >= 1
+// token chunks per rank (chunk c of rank s = its tokens [c*S/C, (c+1)*S/C)).
+// Global token order is (rank, chunk, token), so the global slot of my first
+// chunk-c assignment to e is base = sum of the counts before (rank, c), and the
+// kept rows are clamp(cap - base, 0, count).
+// Owner o's receive buffer is chunk-major, each chunk expert-major:
+//   [chunk c][local expert j][source s][rows in slot order]
+// (C = 1: the single-GPU expert buffer without padding). Outputs per chunk c:
+// slot_base[c][e], row_base[c][e] (my first chunk-c row for e in its owner's
+// buffer), seg_start/seg_rows[c][j] (my buffer as an owner), recv_rows[c].
 __global__ void ep_plan_kernel(const int32_t* __restrict__ counts, int world, int rank, int E,
-                               int64_t cap, int32_t* __restrict__ slot_base,
+                               int C, int64_t cap, int32_t* __restrict__ slot_base,
                                int32_t* __restrict__ row_base, int32_t* __restrict__ seg_start,
                                int32_t* __restrict__ seg_rows, int32_t* __restrict__ recv_rows) {
-  extern __shared__ int kept[];  // [world][E]
+  extern __shared__ int kept[];  // [world][C][E], then chunk_off [world][C]
+  int* chunk_off = kept + world * C * E;
   const int e_loc = E / world;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int64_t base = 0;  // assignments to e on lower ranks: the global slot of my first one
-    for (int s = 0; s < world; ++s) {
-      const int c = counts[s * E + e];
-      int64_t kp = cap - base;
-      kp = kp < 0 ? 0 : (kp > c ? c : kp);
-      kept[s * E + e] = (int)kp;
-      if (s == rank) slot_base[e] = (int)base;
-      base += c;
+    int64_t base = 0;
+    for (int s = 0; s < world; ++s)
+      for (int c = 0; c < C; ++c) {
+        const int cnt = counts[(s * C + c) * E + e];
+        int64_t kp = cap - base;
+        kp = kp < 0 ? 0 : (kp > cnt ? cnt : kp);
+        kept[(s * C + c) * E + e] = (int)kp;
+        if (s == rank) slot_base[c * E + e] = (int)base;
+        base += cnt;
+      }
+  }
+  __syncthreads();
+  // chunk offsets of every owner's buffer
+  for (int i = threadIdx.x; i < world; i += blockDim.x) {
+    int64_t run = 0;
+    for (int c = 0; c < C; ++c) {
+      chunk_off[i * C + c] = (int)run;
+      for (int j = 0; j < e_loc; ++j)
+        for (int s = 0; s < world; ++s) run += kept[(s * C + c) * E + i * e_loc + j];
     }
   }
   __syncthreads();
-  // owner o's receive buffer is expert-major: [local expert j][source s][rows in
-  // slot order] = [local expert][global slot], i.e. the single-GPU expert buffer
-  // without padding. My rows for expert e start at
-  //   sum_{j' < e % e_loc} sum_s kept[s][o*e_loc + j']  +  sum_{s < rank} kept[s][e]
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+  for (int ce = threadIdx.x; ce < C * E; ce += blockDim.x) {
+    const int c = ce / E, e = ce % E;
     const int o = e / e_loc, el = e % e_loc;
-    int64_t st = 0;
+    int64_t st = chunk_off[o * C + c];
     for (int j = 0; j < el; ++j)
-      for (int s = 0; s < world; ++s) st += kept[s * E + o * e_loc + j];
-    for (int s = 0; s < rank; ++s) st += kept[s * E + e];
-    row_base[e] = (int)st;
+      for (int s = 0; s < world; ++s) st += kept[(s * C + c) * E + o * e_loc + j];
+    for (int s = 0; s < rank; ++s) st += kept[(s * C + c) * E + e];
+    row_base[c * E + e] = (int)st;
   }
-  if (threadIdx.x == 0) {  // as an owner: one group per local expert
-    int64_t run = 0;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {  // as an owner: one group per local expert
+    int64_t run = chunk_off[rank * C + c];
+    const int64_t start = run;
     for (int j = 0; j < e_loc; ++j) {
       int64_t r = 0;
-      for (int s = 0; s < world; ++s) r += kept[s * E + rank * e_loc + j];
-      seg_start[j] = (int)run;
-      seg_rows[j] = (int)r;
+      for (int s = 0; s < world; ++s) r += kept[(s * C + c) * E + rank * e_loc + j];
+      seg_start[c * e_loc + j] = (int)run;
+      seg_rows[c * e_loc + j] = (int)r;
       run += r;
     }
-    *recv_rows = (int)run;
+    recv_rows[c] = (int)(run - start);
   }
 }
 
@@ -200,6 +231,7 @@ int launch_pull_rows(int64_t S, int64_t row_bytes, int k, int e_per_rank, const 
   if (S == 0) return 0;
   int64_t g = (S + 7) / 8;
   if (g > 148 * 64) g = 148 * 64;
+  if (comm_block_limit() > 0 && g > comm_block_limit()) g = comm_block_limit();
   if (row_bytes % 16 == 0)
     pull_rows_kernel<uint4><<<(unsigned)g, 256, 0, st>>>(S, row_bytes, k, e_per_rank, ids,
                                                          row_index, peer_rows, out);
@@ -209,13 +241,13 @@ int launch_pull_rows(int64_t S, int64_t row_bytes, int k, int e_per_rank, const 
   return (int)cudaGetLastError();
 }
 
-int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap,
+int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int C, int64_t cap,
                    int32_t* slot_base, int32_t* row_base, int32_t* seg_start, int32_t* seg_rows,
                    int32_t* recv_rows, cudaStream_t st) {
-  const size_t smem = (size_t)world * E * sizeof(int);
+  const size_t smem = ((size_t)world * C * E + (size_t)world * C) * sizeof(int);
   if (smem > 48 * 1024) return MOE_EINVAL;
-  ep_plan_kernel<<<1, 256, smem, st>>>(counts, world, rank, E, cap, slot_base, row_base, seg_start,
-                                       seg_rows, recv_rows);
+  ep_plan_kernel<<<1, 256, smem, st>>>(counts, world, rank, E, C, cap, slot_base, row_base,
+                                       seg_start, seg_rows, recv_rows);
   return (int)cudaGetLastError();
 }
 
@@ -268,8 +300,24 @@ int moe_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap, 
                 void* stream) {
   CHECK(world >= 1 && rank >= 0 && rank < world && E >= world && E % world == 0 && cap >= 0);
   CHECK(counts && slot_base && row_base && seg_start && seg_rows && recv_rows);
-  return moe::launch_ep_plan(counts, world, rank, E, cap, slot_base, row_base, seg_start, seg_rows,
-                             recv_rows, reinterpret_cast<cudaStream_t>(stream));
+  return moe::launch_ep_plan(counts, world, rank, E, 1, cap, slot_base, row_base, seg_start,
+                             seg_rows, recv_rows, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int moe_ep_plan_chunked(const int32_t* counts, int world, int rank, int E, int chunks, int64_t cap,
+                        int32_t* slot_base, int32_t* row_base, int32_t* seg_start,
+                        int32_t* seg_rows, int32_t* recv_rows, void* stream) {
+  CHECK(world >= 1 && rank >= 0 && rank < world && E >= world && E % world == 0 && cap >= 0 &&
+        chunks >= 1 && chunks <= 64);
+  CHECK(counts && slot_base && row_base && seg_start && seg_rows && recv_rows);
+  return moe::launch_ep_plan(counts, world, rank, E, chunks, cap, slot_base, row_base, seg_start,
+                             seg_rows, recv_rows, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int moe_set_launch_limits(int gemm_ctas, int comm_blocks) {
+  CHECK(gemm_ctas >= 0 && comm_blocks >= 0);
+  moe::set_launch_limits(gemm_ctas, comm_blocks);
+  return MOE_OK;
 }
 
 int moe_ipc_barrier(int* const* peer_signal, int* my_signal, int world, int rank,

@@ -1129,6 +1129,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
     attr_done = true;
   }
   int64_t grid = num_sms();
+  if (gemm_cta_limit() > 0 && gemm_cta_limit() < grid) grid = gemm_cta_limit();
   static const int nonpersist = [] {
     const char* v = getenv("MOE_NONPERSIST");
     return v ? atoi(v) : 0;

@@ -67,7 +67,10 @@ int launch_wgrad_bf16(const void* X, int64_t x_rows, int P, const void* Y, int Q
                       int acc, cudaStream_t st);
 
 // expert parallelism over NVLink peer memory (ep_p2p.cu)
-int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap,
+void set_launch_limits(int gemm_ctas, int comm_blocks);
+int gemm_cta_limit();
+int comm_block_limit();
+int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int C, int64_t cap,
                    int32_t* slot_base, int32_t* row_base, int32_t* seg_start, int32_t* seg_rows,
                    int32_t* recv_rows, cudaStream_t st);
 int launch_pull_rows(int64_t S, int64_t row_bytes, int k, int e_per_rank, const int32_t* ids,

@@ -605,7 +605,8 @@ int launch_blelloch_f64(double* tree, int64_t m, cudaStream_t st) {
 int launch_scatter(const ScatterArgs& args, cudaStream_t st) {
   if (args.S == 0) return 0;
   const int threads = 256;
-  const int g = grid_for(args.S, threads / 32, 148 * 64);
+  int g = grid_for(args.S, threads / 32, 148 * 64);
+  if (comm_block_limit() > 0 && g > comm_block_limit()) g = comm_block_limit();
   if (args.row_bytes % 16 == 0)
     scatter_kernel<uint4><<<g, threads, 0, st>>>(args);
   else if (args.row_bytes % 8 == 0)

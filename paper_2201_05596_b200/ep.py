@@ -140,7 +140,8 @@ class EPMoeLayer:
 
     def __init__(self, spec: LayerSpec, gate_w, local_experts, shared=None, group=None,
                  dtype=torch.bfloat16, device=None, transport: str = "auto",
-                 schedule: str = "flat", gpus_per_node: int | None = None) -> None:
+                 schedule: str = "flat", gpus_per_node: int | None = None, chunks: int = 1,
+                 comm_sms: int = 16) -> None:
         if spec.kind != "moe":
             raise ShapeError("EPMoeLayer needs a moe LayerSpec")
         if dtype != torch.bfloat16:
@@ -186,6 +187,12 @@ class EPMoeLayer:
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
         self.schedule = schedule
+        # p2p only: split every rank's tokens into `chunks` so chunk c+1's dispatch and
+        # chunk c-1's return pull run beside chunk c's GEMMs (on `comm_sms` SMs the
+        # GEMMs leave free, from a second stream)
+        if chunks < 1 or (chunks > 1 and transport != "p2p"):
+            raise ValueError("chunks > 1 needs the p2p transport")
+        self.chunks, self.comm_sms = int(chunks), int(comm_sms)
         self.exchanger = Exchanger(group, schedule, gpus_per_node) if transport == "nccl" else None
         self._ws: dict = {}
         self._p2p: dict | None = None
@@ -370,6 +377,8 @@ class EPMoeLayer:
 
     def kept_assignments(self, S: int) -> int:
         if self.transport == "p2p":
+            if self.chunks > 1:
+                return int(self._p2p[S]["kept_c"].sum().item())
             return int(self._ws[S]["kept"].sum().item())
         return int(self.last_plan.kept[self.rank].sum()) if self.last_plan is not None else 0
 
@@ -391,6 +400,7 @@ class EPMoeLayer:
 
         if not hasattr(self, "_epoch_dev"):  # one barrier epoch per layer, shared by all S
             self._epoch_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
+            self._epoch2_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
 
         M, k = self.M, self.k
         cap = self.spec.gating.capacity(S * self.world)
@@ -399,13 +409,15 @@ class EPMoeLayer:
         def al(n):
             return (n + 255) // 256 * 256
 
+        C = self.chunks
         off_recv = 0
         off_tok = off_recv + al(rmax * M * 2)
         off_prob = off_tok + al(rmax * 4)
         off_ret = off_prob + al(rmax * 4)
         off_cnt = off_ret + al(rmax * M * 2)
-        off_sig = off_cnt + al(self.world * self.E * 4)
-        total = off_sig + al(64 * 4)
+        off_sig = off_cnt + al(self.world * C * self.E * 4)
+        off_sig2 = off_sig + al(64 * 4)  # second barrier channel (the comm stream)
+        total = off_sig2 + al(64 * 4)
         region = IpcRegion(total, self.group, self.dev)
         i32 = dict(dtype=torch.int32, device=self.dev)
         G = self.E_loc
@@ -416,14 +428,16 @@ class EPMoeLayer:
             row_prob=region.tensor(off_prob, (rmax,), torch.float32),
             ret=region.tensor(off_ret, (rmax, M), torch.bfloat16),
             signal=region.tensor(off_sig, (64,), torch.int32),
-            counts=region.tensor(off_cnt, (self.world * self.E,), torch.int32),
+            signal2=region.tensor(off_sig2, (64,), torch.int32),
+            counts=region.tensor(off_cnt, (self.world * C * self.E,), torch.int32),
             peer_cnt=region.ptr_table(off_cnt),
             peer_recv=region.ptr_table(off_recv), peer_tok=region.ptr_table(off_tok),
             peer_prob=region.ptr_table(off_prob), peer_ret=region.ptr_table(off_ret),
-            peer_sig=region.ptr_table(off_sig),
-            slot_base=torch.empty(self.E, **i32), row_base=torch.empty(self.E, **i32),
-            seg_start=torch.empty(G, **i32), seg_rows=torch.empty(G, **i32),
-            seg_w=torch.arange(G, **i32), recv_rows=torch.empty(1, **i32),
+            peer_sig=region.ptr_table(off_sig), peer_sig2=region.ptr_table(off_sig2),
+            slot_base=torch.empty(C * self.E, **i32), row_base=torch.empty(C * self.E, **i32),
+            seg_start=torch.empty(C * G, **i32), seg_rows=torch.empty(C * G, **i32),
+            seg_w=torch.arange(G, **i32), recv_rows=torch.empty(C, **i32),
+            totals_c=torch.empty(C * self.E, **i32), kept_c=torch.empty(C * self.E, **i32),
             h=torch.empty((rmax, self.F), dtype=self.dtype, device=self.dev),
             err=torch.zeros(1, **i32),
         )
@@ -431,10 +445,13 @@ class EPMoeLayer:
         self._p2p[S] = st
         return st
 
-    def _barrier(self, st: dict) -> None:
-        _lib.call("moe_ipc_barrier", st["peer_sig"].data_ptr(), st["signal"].data_ptr(),
-                  self.world, self.rank, self._epoch_dev.data_ptr(), st["err"].data_ptr(),
-                  _lib.stream_ptr())
+    def _barrier(self, st: dict, channel: int = 0) -> None:
+        """Flag barrier of every rank on the current stream; channel 1 is the comm
+        stream's (its own signals and epoch, so the two streams never interleave)."""
+        sig, psig, ep = ((st["signal"], st["peer_sig"], self._epoch_dev) if channel == 0 else
+                         (st["signal2"], st["peer_sig2"], self._epoch2_dev))
+        _lib.call("moe_ipc_barrier", psig.data_ptr(), sig.data_ptr(), self.world, self.rank,
+                  ep.data_ptr(), st["err"].data_ptr(), _lib.stream_ptr())
 
     def check_errors(self) -> None:
         """Raise if a peer barrier timed out (call after synchronising)."""
@@ -443,6 +460,8 @@ class EPMoeLayer:
                 raise RuntimeError("expert-parallel peer barrier timed out")
 
     def _forward_p2p(self, x: torch.Tensor, out: torch.Tensor | None, timer):
+        if self.chunks > 1:
+            return self._forward_p2p_chunked(x, out, timer)
         if x.device != self.dev:
             x = x.to(self.dev, non_blocking=True)
         x = x.to(self.dtype).contiguous()
@@ -510,6 +529,125 @@ class EPMoeLayer:
         ph(None)
         return out
 
+    def _forward_p2p_chunked(self, x: torch.Tensor, out: torch.Tensor | None, timer):
+        """p2p forward with every rank's tokens in C chunks, pipelined over two
+        streams: the comm stream dispatches chunk c+1 and pulls chunk c-1's
+        combined rows while the main stream runs chunk c's GEMMs on the SMs the
+        launch limits leave free. Per-row results are the unchunked ones (same
+        kernels on the same rows), so outputs stay bit-identical."""
+        if x.device != self.dev:
+            x = x.to(self.dev, non_blocking=True)
+        x = x.to(self.dtype).contiguous()
+        if x.dim() != 2 or x.shape[1] != self.M:
+            raise ShapeError(f"batch width {tuple(x.shape)} does not match layer hidden {self.M}")
+        S, C, RT = x.shape[0], self.chunks, _lib.ROUTE_TILE
+        if S % (C * RT):
+            raise ValueError(f"{C} chunks need tokens per rank in multiples of {C * RT}")
+        ws = self._workspace(S)
+        st = self._p2p_state(S)
+        E, M, F, k, cap = self.E, self.M, self.F, self.k, st["cap"]
+        Sc, Tc, G = S // C, S // C // RT, self.E_loc
+        main = torch.cuda.current_stream(self.dev)
+        if getattr(self, "_comm", None) is None:
+            # GEMMs on a high-priority stream: when a chunk's GEMM and a copy kernel
+            # become ready together, the block scheduler places the GEMM's CTAs first
+            # and the copy kernel's (capped) blocks land on the SMs left free
+            lo, hi = torch.cuda.Stream.priority_range()
+            self._comm = torch.cuda.Stream(device=self.dev, priority=lo)
+            self._gemm = torch.cuda.Stream(device=self.dev, priority=hi)
+            self._nsm = torch.cuda.get_device_properties(self.dev).multi_processor_count
+        comm, gstream = self._comm, self._gemm
+        ms = _lib.stream_ptr()
+        ids, gp, lr, tc = ws["ids"], ws["gp"], ws["local_rank"], ws["tile_counts"]
+        tof, slots, rix = ws["tile_offsets"], ws["slots"], ws["row_index"]
+        out = torch.empty_like(x) if out is None else out
+        rb = M * x.element_size()
+        if S:
+            _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k, None,
+                      ids.data_ptr(), gp.data_ptr(), lr.data_ptr(), tc.data_ptr(), ms)
+        tot, kep = st["totals_c"], st["kept_c"]
+        for c in range(C):  # per-chunk expert counts
+            _lib.call("moe_plan_scan", tc[c * Tc:].data_ptr(), Sc, E, 2 ** 62, None,
+                      tof[c * Tc:].data_ptr(), tot[c * E:].data_ptr(), kep[c * E:].data_ptr(), ms)
+        _lib.call("moe_ipc_allgather_i32", tot.data_ptr(), C * E, st["peer_cnt"].data_ptr(),
+                  self.world, self.rank, st["peer_sig"].data_ptr(), st["signal"].data_ptr(),
+                  self._epoch_dev.data_ptr(), st["err"].data_ptr(), ms)
+        _lib.call("moe_ep_plan_chunked", st["counts"].data_ptr(), self.world, self.rank, E, C, cap,
+                  st["slot_base"].data_ptr(), st["row_base"].data_ptr(), st["seg_start"].data_ptr(),
+                  st["seg_rows"].data_ptr(), st["recv_rows"].data_ptr(), ms)
+        for c in range(C):  # global slots of each chunk
+            _lib.call("moe_plan_scan", tc[c * Tc:].data_ptr(), Sc, E, cap,
+                      st["slot_base"][c * E:].data_ptr(), tof[c * Tc:].data_ptr(),
+                      tot[c * E:].data_ptr(), kep[c * E:].data_ptr(), ms)
+        R = self.comm_sms
+
+        def dispatch(c, limited):
+            _lib.call("moe_set_launch_limits", 0, R * 8 if limited else 0)
+            _lib.call("moe_dispatch_p2p", x[c * Sc:].data_ptr(), Sc, rb, E, k, cap,
+                      ids[c * Sc:].data_ptr(), lr[c * Sc:].data_ptr(), tof[c * Tc:].data_ptr(),
+                      gp[c * Sc:].data_ptr(), st["slot_base"][c * E:].data_ptr(),
+                      st["row_base"][c * E:].data_ptr(), G, st["peer_recv"].data_ptr(),
+                      st["peer_tok"].data_ptr(), st["peer_prob"].data_ptr(),
+                      slots[c * Sc:].data_ptr(), rix[c * Sc:].data_ptr(),
+                      out[c * Sc:].data_ptr(), _lib.stream_ptr())
+            _lib.call("moe_set_launch_limits", 0, 0)
+            self._barrier(st, channel=1)
+
+        def pull(c, limited):
+            _lib.call("moe_set_launch_limits", 0, R * 8 if limited else 0)
+            _lib.call("moe_pull_rows_p2p", Sc, rb, E, k, ids[c * Sc:].data_ptr(),
+                      rix[c * Sc:].data_ptr(), G, st["peer_ret"].data_ptr(),
+                      out[c * Sc:].data_ptr(), _lib.stream_ptr())
+            _lib.call("moe_set_launch_limits", 0, 0)
+
+        fork = torch.cuda.Event()
+        fork.record(main)
+        comm.wait_event(fork)
+        gstream.wait_event(fork)
+        ev_d = [torch.cuda.Event() for _ in range(C)]
+        ev_g = [torch.cuda.Event() for _ in range(C)]
+        with torch.cuda.stream(comm):
+            dispatch(0, False)
+            ev_d[0].record(comm)
+        try:
+            self._chunk_loop(C, cap, st, dispatch, pull, ev_d, ev_g, comm, gstream, main)
+        finally:
+            torch.cuda.set_stream(main)
+        for s_ in (comm, gstream):
+            join = torch.cuda.Event()
+            join.record(s_)
+            main.wait_event(join)
+        return out
+
+    def _chunk_loop(self, C, cap, st, dispatch, pull, ev_d, ev_g, comm, gstream, main):
+        M, F, G, R = self.M, self.F, self.E_loc, self.comm_sms
+        for c in range(C):
+            gstream.wait_event(ev_d[c])
+            torch.cuda.set_stream(gstream)
+            ms = _lib.stream_ptr()
+            if cap:
+                _lib.call("moe_set_launch_limits", self._nsm - R, 0)
+                _lib.call("moe_grouped_gemm_bf16", st["recv"].data_ptr(), st["rmax"], M,
+                          self.w1.data_ptr(), G * F, F, self.b1.data_ptr(), st["h"].data_ptr(), G,
+                          st["seg_start"][c * G:].data_ptr(), 0, st["seg_rows"][c * G:].data_ptr(),
+                          0, st["seg_w"].data_ptr(), cap, _lib.MOE_ACT_GELU, ms)
+                _lib.call("moe_grouped_gemm_bf16_combine_rows", st["h"].data_ptr(), st["rmax"], F,
+                          self.w2.data_ptr(), G * M, M, self.b2.data_ptr(), G,
+                          st["seg_start"][c * G:].data_ptr(), st["seg_rows"][c * G:].data_ptr(),
+                          st["seg_w"].data_ptr(), cap, st["row_token"].data_ptr(),
+                          st["row_prob"].data_ptr(), st["recv"].data_ptr(), st["ret"].data_ptr(),
+                          ms)
+                _lib.call("moe_set_launch_limits", 0, 0)
+            self._barrier(st, channel=0)
+            ev_g[c].record(gstream)
+            torch.cuda.set_stream(main)
+            with torch.cuda.stream(comm):
+                if c + 1 < C:
+                    dispatch(c + 1, True)
+                    ev_d[c + 1].record(comm)
+                comm.wait_event(ev_g[c])
+                pull(c, c + 1 < C)
+
     def plan(self, S: int):
         """(ids, gate_probs, global slots, plan) of the last forward; for the p2p
         transport the plan is summarised as (cap, expert_load) from device tables."""
@@ -519,6 +657,7 @@ class EPMoeLayer:
 
             st = self._p2p[S]
             load = st["seg_rows"].cpu().numpy()
+            load = load.reshape(self.chunks, self.E_loc).sum(axis=0)
             return ws["ids"], ws["gp"], ws["slots"], SimpleNamespace(cap=st["cap"],
                                                                      expert_load=load)
         return ws["ids"], ws["gp"], ws["slots"], self.last_plan

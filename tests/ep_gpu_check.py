@@ -77,7 +77,7 @@ def run_sliced(S_grp, M, E, k, cf, skew, seed, L):
 
 
 def run_case(S_loc, M, E, k, cf, residual, skew, seed, transport="auto", schedule="flat",
-             gpus_per_node=None):
+             gpus_per_node=None, chunks=1):
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", torch.cuda.current_device())
     spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=residual,
@@ -92,7 +92,7 @@ def run_case(S_loc, M, E, k, cf, residual, skew, seed, transport="auto", schedul
     want = full(x_all)
     ids_f, gp_f, slots_f, load_f, cap_f = full.plan(S_loc * world)
     ep = EPMoeLayer.from_params(spec, params, transport=transport, schedule=schedule,
-                                gpus_per_node=gpus_per_node)
+                                gpus_per_node=gpus_per_node, chunks=chunks)
     lo, hi = rank * S_loc, (rank + 1) * S_loc
     got = ep(x_all[lo:hi].clone())
     got = ep(x_all[lo:hi].clone())  # second call: buffer reuse / slot alternation
@@ -137,6 +137,15 @@ def main():
             dropped = run_case(*c, transport=transport)
             if dist.get_rank() == 0:
                 print(f"ep ok world={world} transport={transport} case={c} "
+                      f"dropped_on_rank0={dropped}", flush=True)
+    # chunked p2p (dispatch / pull of neighbouring chunks beside the GEMMs): bit-identical
+    for c in [(2048, 2048, 32, 1, 1.0, False, 0.0, 3), (2560, 1024, 16, 1, 0.8, False, 1.0, 5)]:
+        for chunks in (2, 4):
+            if c[0] % (chunks * 128):
+                continue
+            dropped = run_case(*c, transport="p2p", chunks=chunks)
+            if dist.get_rank() == 0:
+                print(f"ep ok world={world} transport=p2p-chunked chunks={chunks} case={c} "
                       f"dropped_on_rank0={dropped}", flush=True)
     # hierarchical node/rail schedule (2 "nodes" of world/2 GPUs): bit-identical too
     if world % 2 == 0:

@@ -25,7 +25,8 @@ def test_ep_matches_single_gpu():
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-5000:]
     assert res.stdout.count("transport=nccl") == 5
-    assert res.stdout.count("transport=p2p") == 2
+    assert res.stdout.count("transport=p2p ") == 2
+    assert res.stdout.count("transport=p2p-chunked") == 4
     if n % 2 == 0:
         assert res.stdout.count("schedule=hierarchical") == 3
     assert res.stdout.count("schedule=coordinated") >= 3
