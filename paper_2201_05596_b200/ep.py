@@ -51,7 +51,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .arch import FFN_MULT, DenseFfn, LayerSpec, MoeLayerParams, _grouped_gemm, _Phases, _t
+from .arch import FFN_MULT, DenseFfn, LayerSpec, MoeLayerParams, _Phases, _t
 from .exchange import Exchanger, ReplicaMismatchError
 from .gating import GatingConfig
 from .tensor import ShapeError

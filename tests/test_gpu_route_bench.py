@@ -3,7 +3,6 @@
 checks of the reference's tests/test_cli.py:122-149."""
 
 import csv
-import io
 import json
 import os
 

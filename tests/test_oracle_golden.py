@@ -4,7 +4,6 @@ reference itself (tests/golden/make_golden.py). CPU only."""
 import os
 
 import numpy as np
-import pytest
 
 from oracle import moe_oracle as O
 from tests.conftest import GOLDEN
