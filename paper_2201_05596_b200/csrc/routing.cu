@@ -11,6 +11,8 @@
 #include "common.cuh"
 #include "moe_kernels.h"
 
+#include <cstdlib>
+
 namespace moe {
 
 // ============================================================ top-k gate
