@@ -394,7 +394,10 @@ struct alignas(sizeof(T) * VEC) Pack {
   T v[VEC];
 };
 
-template <typename T, typename P, bool kExpertOrder, int VEC>
+// TPW tokens per warp (32/TPW lanes each): TPW = 2 halves the warps, so 16K
+// tokens fill ~1.7 waves of resident warps instead of ~3.5, while every warp
+// keeps two independent index -> row load chains in flight.
+template <typename T, typename P, bool kExpertOrder, int VEC, int TPW = 1>
 __global__ void combine_kernel(const T* __restrict__ y, int64_t S, int M, int k, int E, int64_t cap,
                                const int32_t* __restrict__ ids, const int32_t* __restrict__ slots,
                                const int32_t* __restrict__ row_index, const P* __restrict__ gp,
@@ -402,11 +405,13 @@ __global__ void combine_kernel(const T* __restrict__ y, int64_t S, int M, int k,
                                T* __restrict__ out) {
   using A = typename Acc<T>::type;
   using V = Pack<T, VEC>;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  constexpr int LPT = 32 / TPW;  // lanes per token
+  const int lane = threadIdx.x & (LPT - 1);
+  const int64_t slots_total = (int64_t)gridDim.x * (blockDim.x >> 5) * TPW;
   const int nv = M / VEC;
-  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
-       t += warps_total) {
+  for (int64_t t = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * TPW +
+                   (threadIdx.x & 31) / LPT;
+       t < S; t += slots_total) {
     int64_t r0 = -1, r1 = -1;
     A p0 = 0, p1 = 0;
     int e0 = 0, e1 = 0, n = 0;
@@ -436,7 +441,7 @@ __global__ void combine_kernel(const T* __restrict__ y, int64_t S, int M, int k,
     const V* sv = reinterpret_cast<const V*>(shared + t * M);
     V* ov = reinterpret_cast<V*>(out + t * M);
 #pragma unroll 4
-    for (int c = lane; c < nv; c += 32) {
+    for (int c = lane; c < nv; c += LPT) {
       V a0, a1, xa, sa;
       if (n > 0) a0 = y0[c];
       if (n > 1) a1 = y1[c];
@@ -625,6 +630,22 @@ static void combine_vec(bool expert_order, int g, int threads, cudaStream_t st, 
                         int64_t S, int M, int k, int E, int64_t cap, const int32_t* ids,
                         const int32_t* slots, const int32_t* row_index, const void* gp,
                         const void* x, const void* shared, void* out) {
+  static const int tpw = [] {
+    const char* v = getenv("MOE_COMBINE_TPW");
+    return v ? atoi(v) : 2;
+  }();
+  if (tpw == 2 && VEC > 1) {
+    const int g2 = (g + 1) / 2;
+    if (expert_order)
+      combine_kernel<T, P, true, VEC, 2><<<g2, threads, 0, st>>>(
+          (const T*)y, S, M, k, E, cap, ids, slots, row_index, (const P*)gp, (const T*)x,
+          (const T*)shared, (T*)out);
+    else
+      combine_kernel<T, P, false, VEC, 2><<<g2, threads, 0, st>>>(
+          (const T*)y, S, M, k, E, cap, ids, slots, row_index, (const P*)gp, (const T*)x,
+          (const T*)shared, (T*)out);
+    return;
+  }
   if (expert_order)
     combine_kernel<T, P, true, VEC><<<g, threads, 0, st>>>(
         (const T*)y, S, M, k, E, cap, ids, slots, row_index, (const P*)gp, (const T*)x,
