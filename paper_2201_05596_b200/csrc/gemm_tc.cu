@@ -261,9 +261,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   // run the other m-blocks of the same n-blocks share each weight tile.
   // args.raster: 0 = plain round robin with m fastest (concurrent clusters share
   // the weight tile), 1 = round robin over runs of 4 n-blocks with n fastest.
-  // raster 2: as 0 (m fastest) but each pair takes runs of 2 tiles: both m-blocks
-  // of a (group, n-block) back to back, the weight tile re-read from L2
-  const int kRun = args.raster == 1 ? 4 : (args.raster == 2 ? 2 : 1);
+  const int kRun = args.raster == 1 ? 4 : 1;
   auto tile_at = [&](int it) {
     return ((it / kRun) * work_stride + work_id) * kRun + (it % kRun);
   };
@@ -1130,14 +1128,6 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   }
   int64_t grid = num_sms();
   if (gemm_cta_limit() > 0 && gemm_cta_limit() < grid) grid = gemm_cta_limit();
-  static const int nonpersist = [] {
-    const char* v = getenv("MOE_NONPERSIST");
-    return v ? atoi(v) : 0;
-  }();
-  // non-persistent: one CTA (pair) per tile, the hardware block scheduler hands
-  // out tiles in order as SMs free up (no drift between the pairs that share a
-  // weight tile)
-  if (nonpersist && EPI != EPI_GATE && max_tiles * CG > grid) grid = max_tiles * CG;
   if (max_tiles * CG < grid) grid = max_tiles < 1 ? CG : max_tiles * CG;
   grid -= grid % CG;
   cudaLaunchConfig_t cfg{};
