@@ -315,6 +315,7 @@ def run_gpu(args):
     # ---- decode (BASELINE config 5): p50 latency of one layer forward for small
     # global batches at the same layer shape (weights streamed from HBM)
     decode = {}
+    decode_roof = {}
     if not args.no_decode:
         for sd in (64, 128, 256, 512):
             s_loc = sd // world
@@ -339,6 +340,12 @@ def run_gpu(args):
             if world > 1:
                 dist.all_reduce(lt, op=dist.ReduceOp.MAX)
             decode[str(sd)] = round(float(lt.median().item()), 4)
+            if world == 1:  # weight bytes the batch actually streams (experts with load > 0)
+                load = layer.plan(s_loc)[3]
+                active = int((load > 0).sum().item())
+                wbytes = active * (2 * M * F * 2 + (F + M) * 4)
+                decode_roof[str(sd)] = {"active_experts": active, "weight_bytes": wbytes,
+                                        "GB_s": round(wbytes / (decode[str(sd)] * 1e-3) / 1e9, 1)}
     # ---- training step (forward saving context + backward), N=1 only: reported
     # beside the inference metric; 12*A*M*F GEMM flops per step
     train = None
@@ -412,6 +419,23 @@ def run_gpu(args):
         dts = [cpu_reference_step(state)[0] for _ in range(3)]
         cpu = {"value": CPU_SAMPLE["S"] / statistics.median(dts), "unit": UNIT, "cores": cores,
                "kind": "port", "sample": cpu_desc() + "; median of 3 after one warm-up"}
+    # HBM-bound components (SURVEY 8(d) formulas, per rank, phase times from the
+    # timed region): achieved GB/s and fraction of the measured HBM peak
+    A_r = kept_rank
+    T_r = (S + 127) // 128
+    epad = max(32, 1 << (E - 1).bit_length())
+    comp_bytes = {"gate": S * M * 2 + epad * M * 2 + S * k * 12 + T_r * E * 4,
+                  "dispatch": 2 * A_r * M * 2,
+                  "combine": (A_r * M + 2 * S * M + (S * M if residual else 0)) * 2}
+    components = {}
+    for name, nbytes in comp_bytes.items():
+        t_ms = phases.get(name)
+        if t_ms:
+            gbs = nbytes / (t_ms * 1e-3) / 1e9
+            components[name] = {"ms": round(t_ms, 4), "bytes": int(nbytes), "GB_s": round(gbs, 1),
+                                "frac_hbm": round(gbs / hbm, 3)}
+    for sd, d in decode_roof.items():
+        d["frac_hbm"] = round(d["GB_s"] / hbm, 3)
     value = S * world / (ms * 1e-3)
     line = {
         "metric": METRIC if args.workload == "c3" else f"MoE-layer fwd tokens/s @{args.workload}",
@@ -434,6 +458,8 @@ def run_gpu(args):
                      "frac_of_burst": achieved / tf_burst if achieved else None},
         "phases_ms": phases,
         "decode_p50_ms": decode or None,
+        "decode_roofline": decode_roof or None,
+        "components": components,
         "train_step": train,
         "kept_assignments_per_gpu": kept_rank,
         "cpu_baseline": cpu,
