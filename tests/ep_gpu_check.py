@@ -138,6 +138,22 @@ def main():
             if dist.get_rank() == 0:
                 print(f"ep ok world={world} transport={transport} case={c} "
                       f"dropped_on_rank0={dropped}", flush=True)
+    # seeded random configurations, both transports where they apply
+    rng = np.random.default_rng(2024 + world)
+    for i in range(4):
+        S_loc = int(rng.integers(1, 40)) * 64 + int(rng.integers(0, 64))
+        M = int(rng.choice([256, 512, 1024]))
+        E = world * int(rng.integers(1, 9))
+        k = 1 if E == 1 else int(rng.choice([1, 2]))
+        cf = float(rng.uniform(0.5, 1.5))
+        residual = bool(rng.random() < 0.3)
+        c = (S_loc, M, E, k, cf, residual, float(rng.uniform(0, 1.5)), 100 + i)
+        for transport in ("nccl", "p2p"):
+            if transport == "p2p" and (k != 1 or residual):
+                continue
+            run_case(*c, transport=transport)
+            if dist.get_rank() == 0:
+                print(f"ep ok world={world} random-case via {transport} case={c}", flush=True)
     # chunked p2p (dispatch / pull of neighbouring chunks beside the GEMMs): bit-identical
     for c in [(2048, 2048, 32, 1, 1.0, False, 0.0, 3), (2560, 1024, 16, 1, 0.8, False, 1.0, 5)]:
         for chunks in (2, 4):

@@ -30,3 +30,4 @@ def test_ep_matches_single_gpu():
     if n % 2 == 0:
         assert res.stdout.count("schedule=hierarchical") == 3
     assert res.stdout.count("schedule=coordinated") >= 3
+    assert res.stdout.count("random-case") >= 4
