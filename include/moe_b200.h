@@ -250,7 +250,7 @@ int moe_grouped_gemm_bf16_wgrad(const void* X, int64_t x_rows, int P, const void
 int moe_gemm_bf16_wgrad_f32(const void* X, int64_t rows, int P, const void* Y, int Q, float* D,
                             void* stream);
 
-/* dx[t] = dout[t] + sum_j kept dxr[ids*cap + slot] + extra1[t] (+ extra2[t]). */
+/* dx[t] = dout[t] + sum_j kept dxr[ids*cap + slot] + extra1[t] (+ extra2[t]); M % 8 == 0. */
 int moe_bwd_dx_bf16(const void* dout, const void* dxr, int64_t S, int M, int E, int k, int64_t cap,
                     const int32_t* ids, const int32_t* slots, const void* extra1,
                     const void* extra2, void* dx, void* stream);

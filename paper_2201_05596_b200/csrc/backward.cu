@@ -150,35 +150,44 @@ __global__ void bwd_dx_kernel(const __nv_bfloat16* __restrict__ dout,
                               const __nv_bfloat16* __restrict__ extra1,
                               const __nv_bfloat16* __restrict__ extra2,
                               __nv_bfloat16* __restrict__ dx) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < S;
-       t += warps_total) {
+  // half-warp per token, 16-B vectors (M % 8 == 0); fp32 sum in the order
+  // dout + dX_e0 + dX_e1 + extra1 + extra2
+  constexpr int LPT = 16;
+  const int lane = threadIdx.x & (LPT - 1);
+  const int64_t slots_total = (int64_t)gridDim.x * (blockDim.x >> 5) * 2;
+  for (int64_t t = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2 +
+                   (threadIdx.x & 31) / LPT;
+       t < S; t += slots_total) {
     int64_t rr[2] = {-1, -1};
     for (int j = 0; j < k; ++j) {
       const int s = slots[t * k + j];
       if (s >= 0) rr[j] = (int64_t)ids[t * k + j] * cap + s;
     }
-    for (int c = lane * 2; c < M; c += 64) {
-      float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + t * M + c));
-      for (int j = 0; j < 2; ++j) {
-        if (rr[j] >= 0) {
-          const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dxr + rr[j] * M + c));
-          v.x += a.x;
-          v.y += a.y;
+    for (int c = lane * 8; c < M; c += LPT * 8) {
+      float v[8];
+      auto acc = [&](const __nv_bfloat16* p, bool first) {
+        const uint4 q = *reinterpret_cast<const uint4*>(p);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          v[2 * i] = first ? f.x : v[2 * i] + f.x;
+          v[2 * i + 1] = first ? f.y : v[2 * i + 1] + f.y;
         }
+      };
+      acc(dout + t * M + c, true);
+      for (int j = 0; j < 2; ++j)
+        if (rr[j] >= 0) acc(dxr + rr[j] * M + c, false);
+      if (extra1) acc(extra1 + t * M + c, false);
+      if (extra2) acc(extra2 + t * M + c, false);
+      uint4 o;
+      uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        op[i] = *reinterpret_cast<const uint32_t*>(&b);
       }
-      if (extra1) {
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(extra1 + t * M + c));
-        v.x += a.x;
-        v.y += a.y;
-      }
-      if (extra2) {
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(extra2 + t * M + c));
-        v.x += a.x;
-        v.y += a.y;
-      }
-      *reinterpret_cast<__nv_bfloat162*>(dx + t * M + c) = __floats2bfloat162_rn(v.x, v.y);
+      *reinterpret_cast<uint4*>(dx + t * M + c) = o;
     }
   }
 }
@@ -275,10 +284,11 @@ int moe_gemm_bf16_wgrad_f32(const void* X, int64_t rows, int P, const void* Y, i
 int moe_bwd_dx_bf16(const void* dout, const void* dxr, int64_t S, int M, int E, int k, int64_t cap,
                     const int32_t* ids, const int32_t* slots, const void* extra1,
                     const void* extra2, void* dx, void* stream) {
-  CHECK(S >= 0 && M >= 2 && M % 2 == 0 && E >= 1 && (k == 1 || k == 2) && cap >= 0);
+  CHECK(S >= 0 && M >= 8 && M % 8 == 0 && E >= 1 && (k == 1 || k == 2) && cap >= 0);
   if (S == 0) return MOE_OK;
   CHECK(dout && ids && slots && dx && (cap == 0 || dxr));
-  moe::bwd_dx_kernel<<<moe::grid_warps(S), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  moe::bwd_dx_kernel<<<(moe::grid_warps(S) + 1) / 2, 256, 0,
+                       reinterpret_cast<cudaStream_t>(stream)>>>(
       (const __nv_bfloat16*)dout, (const __nv_bfloat16*)dxr, S, M, k, cap, ids, slots,
       (const __nv_bfloat16*)extra1, (const __nv_bfloat16*)extra2, (__nv_bfloat16*)dx);
   return (int)cudaGetLastError();
