@@ -354,6 +354,18 @@ MOE_DEV void tma_load_2d_cg2(void* smem_dst, const CUtensorMap* map, uint64_t* b
       : "memory");
 }
 
+// 2-CTA TMA load multicast to the CTAs in cta_mask (same smem offset in each);
+// each destination's bytes are signalled on its pair leader's barrier.
+MOE_DEV void tma_load_2d_cg2_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                int32_t c0, int32_t c1, uint16_t cta_mask) {
+  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "h"(cta_mask), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 MOE_DEV void tma_load_2d_cg2_hint(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
                                   int32_t c1, uint64_t policy) {
   const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;

@@ -155,7 +155,10 @@ constexpr int out_stage_bytes() {
              ? EW * out_bufs<BN>() * 2048 : 0;
 }
 
-template <int BN, int STAGES, int EPI, int CG, int EW>
+// CL = cluster size: CG (one CTA pair per cluster) or 2*CG = 4: two pairs run the
+// two m-blocks of the same (group, n-block) and share the weight tile, each CTA
+// loading half of it and multicasting to its counterpart in the other pair.
+template <int BN, int STAGES, int EPI, int CG, int EW, int CL = CG>
 __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
@@ -186,9 +189,15 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   const uint32_t lane = lane_id();
   const int G = args.G;
   const int n_blocks = (args.N + BN - 1) / BN;
-  const uint32_t cta = CG == 2 ? cluster_ctarank() : 0;  // rank inside the CTA pair
+  static_assert(CL == CG || (CG == 2 && CL == 4), "cluster = one pair or two pairs");
+  constexpr int CLP = CL / CG;  // CTA pairs per cluster
+  constexpr int TMC = TM * CLP;  // rows per cluster tile
+  const uint32_t qrank = CL > 1 ? cluster_ctarank() : 0;
+  const uint32_t cta = qrank % CG;    // rank inside the CTA pair
+  const uint32_t pair = qrank / CG;   // pair inside the cluster
+  const uint32_t pl = qrank - cta;    // this pair's leader CTA
   const bool leader = cta == 0;
-  const int work_id = blockIdx.x / CG, work_stride = gridDim.x / CG;
+  const int work_id = blockIdx.x / CL, work_stride = gridDim.x / CL;
   if constexpr (CG == 2) cluster_sync();  // both CTAs resident before the paired TMEM alloc
 
   // ---- per-CTA tile table: tile_start[g] = sum_{g'<g} ceil(rows/TM) * n_blocks
@@ -198,7 +207,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     int local = 0;
     for (int g = g0; g < min(G, g0 + per); ++g) {
       const int64_t r = args.rows ? args.rows[g] : args.rows_const;
-      local += (int)((r + TM - 1) / TM) * n_blocks;
+      local += (int)((r + TMC - 1) / TMC) * n_blocks;
     }
     int incl = local;
 #pragma unroll
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     for (int g = g0; g < min(G, g0 + per); ++g) {
       tile_start[g] = run;
       const int64_t r = args.rows ? args.rows[g] : args.rows_const;
-      run += (int)((r + TM - 1) / TM) * n_blocks;
+      run += (int)((r + TMC - 1) / TMC) * n_blocks;
     }
     if (lane == 31) tile_start[G] = incl;
   }
@@ -218,7 +227,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     if (lane == 0) {
       for (int s = 0; s < STAGES; ++s) {
         mbar_init(&full[s], CG);  // CG=2: the peer's producer arrives remotely on the leader's
-        mbar_init(&empty[s], 1);
+        mbar_init(&empty[s], CLP);  // CL=4: both pairs' MMAs release every stage
       }
       for (int a = 0; a < AS; ++a) {
         mbar_init(&tfull[a], 1);
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       mb = local / n_blocks;
       nb = local - mb * n_blocks;
     } else {
-      const int mblocks = (int)((r + TM - 1) / TM);
+      const int mblocks = (int)((r + TMC - 1) / TMC);
       nb = local / mblocks;
       mb = local - nb * mblocks;
     }
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
-      const int a_row = (int)(rs + (int64_t)mb * TM + cta * BM);
+      const int a_row = (int)(rs + (int64_t)mb * TMC + pair * TM + cta * BM);
       const int b_row = w * args.N + nb * BN + cta * (BN / CG);
       // gather mode: this lane's 4 source rows of the CTA's 128-row A tile (rows past
       // the group's count read row 0: their outputs are padding)
@@ -347,7 +356,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         const int64_t rg = args.rows ? args.rows[g] : args.rows_const;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int64_t lr = (int64_t)mb * TM + cta * BM + 4 * lane + i;
+          const int64_t lr = (int64_t)mb * TMC + pair * TM + cta * BM + 4 * lane + i;
           grow[i] = lr < rg ? args.a_gather[rs + lr] : 0;
         }
       }
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
                 if (leader)
                   mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
                 else
-                  mbar_arrive_cluster(&full[stage], 0);
+                  mbar_arrive_cluster(&full[stage], pl);
               } else {
                 mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
 #pragma unroll
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               if (leader)
                 mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
               else
-                mbar_arrive_cluster(&full[stage], 0);
+                mbar_arrive_cluster(&full[stage], pl);
             }
           } else {
             if (lane == 0) mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
@@ -468,14 +477,25 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             if (leader)
               mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
             else
-              mbar_arrive_cluster(&full[stage], 0);
+              mbar_arrive_cluster(&full[stage], pl);
+          } else if constexpr (CL == 4) {
+            // weight tile shared by both pairs: load my half of my 128 B rows and
+            // multicast it to my counterpart in the other pair (same cta index)
+            tma_load_2d_cg2(sa, &map_a, &full[stage], kb * BK, a_row);
+            constexpr int kHalf = BN / CG / CLP;  // B rows per multicast box
+            tma_load_2d_cg2_mc(sb + pair * kHalf * BK * 2, &map_b, &full[stage], kb * BK,
+                               b_row + pair * kHalf, (uint16_t)((1u << cta) | (1u << (cta + 2))));
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+            else
+              mbar_arrive_cluster(&full[stage], pl);
           } else if constexpr (CG == 2) {
             tma_load_2d_cg2(sa, &map_a, &full[stage], kb * BK, a_row);
             tma_load_2d_cg2(sb, &map_b, &full[stage], kb * BK, b_row);
             if (leader)
               mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
             else
-              mbar_arrive_cluster(&full[stage], 0);
+              mbar_arrive_cluster(&full[stage], pl);
           } else {
             mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
             tma_load_2d(sa, &map_a, &full[stage], kb * BK, a_row);
@@ -537,7 +557,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             }
           }
           if constexpr (CG == 2)
-            umma_commit_cg2(&empty[stage], 0x3);  // frees the stage in both CTAs
+            umma_commit_cg2(&empty[stage], CL == 4 ? 0xF : 0x3);  // frees the stage (all CTAs that wrote it)
           else
             umma_commit(&empty[stage]);
         }
@@ -549,7 +569,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       }
       if (lane == 0) {
         if constexpr (CG == 2)
-          umma_commit_cg2(&tfull[acc], 0x3);
+          umma_commit_cg2(&tfull[acc], (uint16_t)(0x3u << pl));
         else
           umma_commit(&tfull[acc]);
       }
@@ -565,7 +585,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     constexpr int kColSplit = EW / 4;    // warps sharing a quarter split the columns
     const int col_part = (int)(warp - 2) / 4;          // 0 .. kColSplit-1
     constexpr int kChunks = BN / 32 / kColSplit;       // 32-column chunks per warp
-    const int row_in_tile = cta * BM + quarter * 32 + lane;
+    const int row_in_tile = pair * TM + cta * BM + quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
     int g = 0;
@@ -588,7 +608,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int64_t rows_g = args.rows ? args.rows[g] : args.rows_const;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
-      const int64_t local_row = (int64_t)mb * TM + row_in_tile;
+      const int64_t local_row = (int64_t)mb * TMC + row_in_tile;
       const bool valid = local_row < rows_g;
       const int64_t out_row = rs + local_row;
       bool kzero = false;  // weight gradient of a group with no rows: zeros, TMEM not written
@@ -667,7 +687,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(&map_d, ob, col0, (int)(mb * TM + cta * BM + quarter * 32), g);
+              tma_store_3d(&map_d, ob, col0, (int)(mb * TMC + row_in_tile - lane), g);
               bulk_commit_group();
             }
             ++ostage;
@@ -798,7 +818,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         __syncwarp();
         if (lane == 0) {
           if constexpr (CG == 2)
-            mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA reuses this accumulator
+            mbar_arrive_cluster(&tempty[acc], pl);  // the leader's MMA reuses this accumulator
           else
             mbar_arrive(&tempty[acc]);
         }
@@ -880,7 +900,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         __syncwarp();
         if (lane == 0) {
           if constexpr (CG == 2)
-            mbar_arrive_cluster(&tempty[acc], 0);
+            mbar_arrive_cluster(&tempty[acc], pl);
           else
             mbar_arrive(&tempty[acc]);
         }
@@ -987,7 +1007,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               if (leader)
                 mbar_arrive(&full[stage]);
               else
-                mbar_arrive_cluster_release(&full[stage], 0);
+                mbar_arrive_cluster_release(&full[stage], pl);
             } else {
               mbar_arrive(&full[stage]);
             }
@@ -1115,11 +1135,11 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4>
+template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4, int CL = CG>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
                      int64_t max_tiles, cudaStream_t st, const CUtensorMap* md = nullptr) {
   using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>()>;
-  auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW>;
+  auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW, CL>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
@@ -1128,8 +1148,9 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   }
   int64_t grid = num_sms();
   if (gemm_cta_limit() > 0 && gemm_cta_limit() < grid) grid = gemm_cta_limit();
-  if (max_tiles * CG < grid) grid = max_tiles < 1 ? CG : max_tiles * CG;
-  grid -= grid % CG;
+  // max_tiles counts cluster tiles (CL/CG pairs each)
+  if (max_tiles * CL < grid) grid = max_tiles < 1 ? CL : max_tiles * CL;
+  grid -= grid % CL;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(threads_for<EW, EPI>());
@@ -1137,11 +1158,22 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if constexpr (CL > 2) {
+    // 4-CTA clusters must fit whole GPCs: size the persistent grid to what can be resident
+    static int max_clusters = 0;
+    if (max_clusters == 0) {
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess ||
+          max_clusters < 1)
+        max_clusters = (int)(num_sms() / CL);
+    }
+    if (grid > (int64_t)max_clusters * CL) grid = (int64_t)max_clusters * CL;
+    cfg.gridDim = dim3((unsigned)grid);
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, md ? *md : mb, args);
   return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
@@ -1267,6 +1299,22 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
       const int64_t tiles512 = (int64_t)G * ((max_group_rows + tm - 1) / tm) * ((N + 511) / 512);
       return gelu ? launch_tc<512, 4, EPI_BIAS_GELU, 2, 8>(ma, mb2, a, tiles512, st, &md)
                   : launch_tc<512, 4, EPI_BIAS, 2, 8>(ma, mb2, a, tiles512, st, &md);
+    }
+    static const int cluster4 = [] {
+      const char* v = getenv("MOE_CLUSTER4");
+      return v ? atoi(v) : 0;
+    }();
+    if (cluster4 && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
+        (N % 8) == 0 && a_gather == nullptr && make_map_out3d(&md, D, G, per_group, N) == 0) {
+      // two CTA pairs per cluster (m-blocks 2j, 2j+1) sharing the weight tile by multicast
+      CUtensorMap mb4;
+      rc = make_map(&mb4, B, b_rows, K, BN / CG / 2);
+      if (rc) return rc;
+      a.tma_store = 1;
+      a.tile_counter = nullptr;  // static schedule: the pairs of a cluster move in step anyway
+      const int64_t tiles4 = (int64_t)G * ((max_group_rows + 2 * tm - 1) / (2 * tm)) * nblk;
+      return gelu ? launch_tc<256, 5, EPI_BIAS_GELU, 2, 8, 4>(ma, mb4, a, tiles4, st, &md)
+                  : launch_tc<256, 5, EPI_BIAS, 2, 8, 4>(ma, mb4, a, tiles4, st, &md);
     }
     if (tma_epi && pad_scratch && row_start == nullptr && per_group > 0 && (N % 8) == 0 &&
         make_map_out3d(&md, D, G, per_group, N) == 0) {
