@@ -22,6 +22,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC", "-shared",
     "--expt-relaxed-constexpr",
     "-Xptxas", "-v",
+    "--threads", "0",  # compile the .cu files in parallel
 ]
 
 
