@@ -103,6 +103,9 @@ def probe(name, fn, secs=2.0):
 
 import os  # noqa: E402
 
+if os.environ.get("PROBE_GEMM_CTAS"):  # cap the persistent GEMM grid (SM-count experiments)
+    _lib.call("moe_set_launch_limits", int(os.environ["PROBE_GEMM_CTAS"]), 0)
+
 SETS = {
     "all": (("grouped_gemm1_gelu", g1), ("grouped_gemm1_gelu_tma", g1t), ("cublas_bmm1_per_expert_w", bb1),
             ("grouped_gemm2", g2), ("grouped_gemm2_tma", g2t), ("cublas_bmm2_per_expert_w", bb2),
