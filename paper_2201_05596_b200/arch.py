@@ -239,15 +239,21 @@ class MoeLayer:
             raise ShapeError("expert weight shapes do not match the spec")
         self.b1 = torch.stack([_t(p.b1, dev, torch.float32).reshape(F) for p in params.experts])
         self.b2 = torch.stack([_t(p.b2, dev, torch.float32).reshape(M) for p in params.experts])
+        # E > 256 (beyond one tcgen05 N tile of the fused gate): logits from the fp32
+        # grouped GEMM on the bf16-rounded x and W_g, then the stand-alone top-k /
+        # plan-tiles kernels, as on the fp32 path; the expert GEMMs stay tcgen05
+        self.wide_gate = self.dtype == torch.bfloat16 and E > 256
         if self.dtype == torch.bfloat16:
-            if E > 256:
-                raise ValueError("the bf16 tcgen05 gate supports E <= 256")
             if M % 8:
                 raise ValueError("the bf16 tensor-core path needs hidden % 8 == 0")
             self.epad = max(32, 1 << (E - 1).bit_length())
-            wg_t = torch.zeros((self.epad, M), dtype=torch.bfloat16, device=dev)
-            wg_t[:E] = gw.t().to(torch.bfloat16)
-            self.wg = wg_t
+            if self.wide_gate:
+                self.wg = None
+                self.wg32 = gw.to(torch.bfloat16).float().contiguous()  # (M, E)
+            else:
+                wg_t = torch.zeros((self.epad, M), dtype=torch.bfloat16, device=dev)
+                wg_t[:E] = gw.t().to(torch.bfloat16)
+                self.wg = wg_t
             self.w1 = w1.transpose(1, 2).reshape(E * F, M).contiguous().to(torch.bfloat16)
             self.w2 = w2.transpose(1, 2).reshape(E * M, F).contiguous().to(torch.bfloat16)
         else:
@@ -294,7 +300,7 @@ class MoeLayer:
             h=torch.empty((max(E * cap, 1), F), dtype=dt, device=dev),
             y=torch.empty((max(E * cap, 1), M), dtype=dt, device=dev),
         )
-        if dt == torch.float32:
+        if dt == torch.float32 or self.wide_gate:
             ws["logits"] = torch.empty((S, E), dtype=torch.float32, device=dev)
         ws["probsum"] = torch.zeros(E, dtype=torch.float32, device=dev)
         ws["aux"] = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -356,7 +362,7 @@ class MoeLayer:
         ph = _Phases(timer)
         ph("gate")
         aux = self.aux_loss
-        if self.dtype == torch.bfloat16:
+        if self.dtype == torch.bfloat16 and not self.wide_gate:
             if aux:
                 ws["probsum"].zero_()
                 _lib.call("moe_gate_gemm_bf16_stats", x.data_ptr(), self.wg.data_ptr(), S, M, E,
@@ -368,8 +374,12 @@ class MoeLayer:
                           tc.data_ptr(), st)
         else:
             logits = ws["logits"] if logits_out is None else logits_out
-            _grouped_gemm(self.dtype, x, S, M, self.wg, E, None, logits, 1, None, 0, None, S, S,
-                          _lib.MOE_ACT_NONE)
+            if self.wide_gate:
+                _grouped_gemm(torch.float32, x.float(), S, M, self.wg32, E, None, logits, 1, None,
+                              0, None, S, S, _lib.MOE_ACT_NONE)
+            else:
+                _grouped_gemm(self.dtype, x, S, M, self.wg, E, None, logits, 1, None, 0, None, S,
+                              S, _lib.MOE_ACT_NONE)
             probs = None
             if aux:
                 probs = ws.setdefault("probs", torch.empty((S, E), dtype=torch.float32,
@@ -381,7 +391,7 @@ class MoeLayer:
         _lib.call("moe_plan_scan", tc.data_ptr(), S, E, cap, None, ws["tile_offsets"].data_ptr(),
                   ws["totals"].data_ptr(), ws["load"].data_ptr(), st)
         if aux:
-            if self.dtype == torch.bfloat16:
+            if self.dtype == torch.bfloat16 and not self.wide_gate:
                 _lib.call("moe_load_balance_loss_from_stats", ws["totals"].data_ptr(),
                           ws["probsum"].data_ptr(), S, E, k, ws["aux"].data_ptr(), st)
             else:

@@ -77,6 +77,8 @@ def forward_train(layer, x: torch.Tensor) -> torch.Tensor:
     """Forward that saves the backward context (bf16 only)."""
     if layer.dtype != torch.bfloat16:
         raise NotImplementedError("the training path is bf16 (tcgen05)")
+    if getattr(layer, "wide_gate", False):
+        raise NotImplementedError("the training path covers E <= 256 (the fused tcgen05 gate)")
     x = x.to(device=layer.device, dtype=layer.dtype).contiguous()
     S = x.shape[0]
     ws = layer.workspace(S)

@@ -325,6 +325,21 @@ def test_bf16_odd_expert_counts(E, k, cf, M):
     close(out.float().cpu().numpy(), want, 2e-2)
 
 
+@pytest.mark.parametrize("E,k,cf", [(300, 1, 1.0), (512, 2, 1.25), (257, 1, 0.7)])
+def test_bf16_wide_gate(E, k, cf):
+    """E > 256: fp32 logits GEMM + stand-alone top-k / plan kernels, tcgen05 experts."""
+    S, M = 2000, 64
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, k, cf))
+    p = rounded_params(spec, E + k, torch.bfloat16)
+    x64 = torch.randn(S, M, generator=torch.Generator().manual_seed(E)).to(torch.bfloat16).double().numpy()
+    layer, x, out, logits = run_layer(spec, p, x64, torch.bfloat16)
+    assert layer.wide_gate
+    lg, _ = check_routing(layer, logits, spec, S)
+    ex, sh = oracle_args(p)
+    want = O.forward_layer_with_logits(x64, lg, ex, sh, E, k, cf)
+    close(out.float().cpu().numpy(), want, 2e-2)
+
+
 def test_bf16_limits_raise():
     spec = A.LayerSpec(kind="moe", hidden=64, experts=300, gating=GatingConfig(300, 1, 1.0))
     p = A.init_layer_params(A.LayerSpec(kind="moe", hidden=8, experts=2, gating=GatingConfig(2)),
