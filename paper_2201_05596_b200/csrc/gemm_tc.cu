@@ -158,7 +158,9 @@ constexpr int out_stage_bytes() {
 // CL = cluster size: CG (one CTA pair per cluster) or 2*CG = 4: two pairs run the
 // two m-blocks of the same (group, n-block) and share the weight tile, each CTA
 // loading half of it and multicasting to its counterpart in the other pair.
-template <int BN, int STAGES, int EPI, int CG, int EW, int CL = CG>
+// SUB: m-blocks a pair runs per scheduled tile (1, or 2 for the 2-CTA instance that
+// shares a cluster-4 launch's tile pool, whose tiles span two m-blocks).
+template <int BN, int STAGES, int EPI, int CG, int EW, int CL = CG, int SUB = 1>
 __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   const int n_blocks = (args.N + BN - 1) / BN;
   static_assert(CL == CG || (CG == 2 && CL == 4), "cluster = one pair or two pairs");
   constexpr int CLP = CL / CG;  // CTA pairs per cluster
-  constexpr int TMC = TM * CLP;  // rows per cluster tile
+  constexpr int TMC = TM * CLP * SUB;  // rows per scheduled tile
   const uint32_t qrank = CL > 1 ? cluster_ctarank() : 0;
   const uint32_t cta = qrank % CG;    // rank inside the CTA pair
   const uint32_t pair = qrank / CG;   // pair inside the cluster
@@ -239,7 +241,8 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       constexpr int kFix = kMN ? 1 : 0;
       for (int q = 0; q < kTileQ; ++q) {
         mbar_init(&tq_full[q], 1);
-        mbar_init(&tq_empty[q], CG == 2 ? 2 + 2 * EW + 2 * kFix : 1 + EW + kFix);
+        // the other CTAs' producers, the pairs' MMA warps, every epilogue / fix-up warp
+        mbar_init(&tq_empty[q], (CL - 1) + CLP + (EW + kFix) * CL);
       }
       mbar_fence_init();
     }
@@ -310,9 +313,10 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         t = claimed < total_tiles ? claimed : -1;
         if (t >= 0) claimed = atomicAdd(args.tile_counter, 1);
         tq[slot] = t;
-        if constexpr (CG == 2) {
-          st_shared_cluster_i32(const_cast<int*>(&tq[slot]), 1, t);
-          mbar_arrive_cluster_release(&tq_full[slot], 1);
+#pragma unroll
+        for (int r = 1; r < CL; ++r) {  // every other CTA of the cluster
+          st_shared_cluster_i32(const_cast<int*>(&tq[slot]), r, t);
+          mbar_arrive_cluster_release(&tq_full[slot], r);
         }
         mbar_arrive(&tq_full[slot]);
       }
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       t = tq[slot];
       __syncwarp();
       if (lane == 0) {
-        if (CG == 2 && !leader)
+        if (qrank != 0)
           mbar_arrive_cluster_release(&tq_empty[slot], 0);
         else
           mbar_arrive(&tq_empty[slot]);
@@ -340,14 +344,19 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     // (L2 eviction-priority hints on A/B were measured and removed: evict_first
     // on the weights raised DRAM traffic from 6.2 to 9.1 GB per GEMM1 launch)
     int gp = 0;  // group cursor for the prefetch look-ahead
-    for (int it = 0;; ++it) {
-      const int tile = fetch(it, leader);
+    int cur = -1;
+    for (int vit = 0;; ++vit) {
+      const int sub = vit % SUB;
+      if (sub == 0) cur = fetch(vit / SUB, qrank == 0);
+      const int tile = cur;
+      const int it = vit / SUB;
       if (tile < 0) break;
       int mb, nb;
       decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
-      const int a_row = (int)(rs + (int64_t)mb * TMC + pair * TM + cta * BM);
+      const int mrow = mb * TMC + (int)(pair * SUB + sub) * TM;  // this pair's m-block
+      const int a_row = (int)(rs + (int64_t)mrow + cta * BM);
       const int b_row = w * args.N + nb * BN + cta * (BN / CG);
       // gather mode: this lane's 4 source rows of the CTA's 128-row A tile (rows past
       // the group's count read row 0: their outputs are padding)
@@ -356,7 +365,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         const int64_t rg = args.rows ? args.rows[g] : args.rows_const;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int64_t lr = (int64_t)mb * TMC + pair * TM + cta * BM + 4 * lane + i;
+          const int64_t lr = (int64_t)mrow + cta * BM + 4 * lane + i;
           grow[i] = lr < rg ? args.a_gather[rs + lr] : 0;
         }
       }
@@ -521,8 +530,10 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     uint32_t acc_phase = 0;
     const int num_kb = (args.K + BK - 1) / BK;
     int g = 0;
-    for (int it = 0; leader; ++it) {
-      const int tile = fetch(it, false);
+    int cur = -1;
+    for (int vit = 0; leader; ++vit) {
+      if (vit % SUB == 0) cur = fetch(vit / SUB, false);
+      const int tile = cur;
       if (tile < 0) break;
       int kb_end = num_kb;
       if constexpr (kMN) {
@@ -600,15 +611,18 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         named_bar_sync(1, 128);
       }
     }
-    for (int it = 0;; ++it) {
-      const int tile = fetch(it, false);
+    int cur = -1;
+    for (int vit = 0;; ++vit) {
+      const int sub = vit % SUB;
+      if (sub == 0) cur = fetch(vit / SUB, false);
+      const int tile = cur;
       if (tile < 0) break;
       int mb, nb;
       decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int64_t rows_g = args.rows ? args.rows[g] : args.rows_const;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
-      const int64_t local_row = (int64_t)mb * TMC + row_in_tile;
+      const int64_t local_row = (int64_t)mb * TMC + sub * TM + row_in_tile;
       const bool valid = local_row < rows_g;
       const int64_t out_row = rs + local_row;
       bool kzero = false;  // weight gradient of a group with no rows: zeros, TMEM not written
@@ -687,7 +701,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(&map_d, ob, col0, (int)(mb * TMC + row_in_tile - lane), g);
+              tma_store_3d(&map_d, ob, col0, (int)(mb * TMC + sub * TM + row_in_tile - lane), g);
               bulk_commit_group();
             }
             ++ostage;
@@ -1095,12 +1109,12 @@ static int prefetch_mode() {
 // tiles, where keeping the weight-sharing pairs in step pays: GEMM2 1.65 vs
 // 1.70 ms in the C3 layer); 1: every launch (GEMM1, 4x more and shorter tiles,
 // loses 2-4% to the queue hand-off); 0: static round robin everywhere.
-static int* dyn_counter(cudaStream_t st, int64_t K = 0, int64_t N = 0) {
+static int* dyn_counter(cudaStream_t st, int64_t K = 0, int64_t N = 0, bool force = false) {
   static const int enabled = [] {
     const char* v = getenv("MOE_DYN_SCHED");
     return v ? atoi(v) : 2;
   }();
-  if (!enabled || (enabled == 2 && K < 2 * N)) return nullptr;
+  if (!force && (!enabled || (enabled == 2 && K < 2 * N))) return nullptr;
   constexpr int kPool = 4096;
   static int* pool[64] = {};
   static unsigned next[64] = {};
@@ -1125,6 +1139,26 @@ static int* dyn_counter(cudaStream_t st, int64_t K = 0, int64_t N = 0) {
   return c;
 }
 
+// A per-device side stream + fork/join events for the hybrid GEMM launch.
+static bool side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join) {
+  static cudaStream_t streams[64] = {};
+  static cudaEvent_t forks[64] = {}, joins[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  if (streams[dev] == nullptr) {
+    if (cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming) != cudaSuccess)
+      return false;
+  }
+  *s = streams[dev];
+  *fork = forks[dev];
+  *join = joins[dev];
+  return true;
+}
+
 static int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -1135,11 +1169,12 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4, int CL = CG>
+template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4, int CL = CG, int SUB = 1>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
-                     int64_t max_tiles, cudaStream_t st, const CUtensorMap* md = nullptr) {
+                     int64_t max_tiles, cudaStream_t st, const CUtensorMap* md = nullptr,
+                     int64_t grid_cap = 0) {
   using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>()>;
-  auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW, CL>;
+  auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW, CL, SUB>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
@@ -1148,6 +1183,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   }
   int64_t grid = num_sms();
   if (gemm_cta_limit() > 0 && gemm_cta_limit() < grid) grid = gemm_cta_limit();
+  if (grid_cap > 0 && grid_cap < grid) grid = grid_cap;
   // max_tiles counts cluster tiles (CL/CG pairs each)
   if (max_tiles * CL < grid) grid = max_tiles < 1 ? CL : max_tiles * CL;
   grid -= grid % CL;
@@ -1176,6 +1212,32 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, md ? *md : mb, args);
   return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
+}
+
+// Resident 4-CTA clusters of the forward GEMM (B200: 33 -> 132 of 148 SMs).
+static int max_clusters4(bool gelu) {
+  static int n[2] = {0, 0};
+  int& v = n[gelu ? 1 : 0];
+  if (v == 0) {
+    using L = Smem<256, 5, 2, out_stage_bytes<EPI_BIAS, 8, 2, 256>()>;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(4 * 64);
+    cfg.blockDim = dim3(threads_for<8, EPI_BIAS>());
+    cfg.dynamicSmemBytes = L::kTotal;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 4;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    auto kern = gelu ? gemm_bf16_tc_kernel<256, 5, EPI_BIAS_GELU, 2, 8, 4>
+                     : gemm_bf16_tc_kernel<256, 5, EPI_BIAS, 2, 8, 4>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    if (cudaOccupancyMaxActiveClusters(&v, kern, &cfg) != cudaSuccess || v < 1)
+      v = num_sms() / 4;
+  }
+  return v;
 }
 
 int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
@@ -1304,7 +1366,38 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
       const char* v = getenv("MOE_CLUSTER4");
       return v ? atoi(v) : 0;
     }();
-    if (cluster4 && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
+    if (cluster4 == 2 && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
+        (N % 8) == 0 && a_gather == nullptr && make_map_out3d(&md, D, G, per_group, N) == 0) {
+      // hybrid: the 4-CTA clusters that fit (weight tile multicast across two pairs)
+      // plus a 2-CTA instance on the SMs they leave, both pulling two-m-block tiles
+      // from one dynamic counter; the instances run on two streams (fork / join)
+      CUtensorMap mb4;
+      rc = make_map(&mb4, B, b_rows, K, BN / CG / 2);
+      if (rc) return rc;
+      a.tma_store = 1;
+      a.tile_counter = dyn_counter(st, 0, 0, true);
+      const int64_t tiles4 = (int64_t)G * ((max_group_rows + 2 * tm - 1) / (2 * tm)) * nblk;
+      int nclus = max_clusters4(gelu);
+      const int64_t left = num_sms() - 4 * (int64_t)nclus;
+      if (a.tile_counter == nullptr || left < 2)
+        return gelu ? launch_tc<256, 5, EPI_BIAS_GELU, 2, 8, 4>(ma, mb4, a, tiles4, st, &md)
+                    : launch_tc<256, 5, EPI_BIAS, 2, 8, 4>(ma, mb4, a, tiles4, st, &md);
+      cudaStream_t side;
+      cudaEvent_t fork, join;
+      if (!side_stream(&side, &fork, &join)) return MOE_EINVAL;
+      cudaEventRecord(fork, st);
+      cudaStreamWaitEvent(side, fork, 0);
+      int r1 = gelu ? launch_tc<256, 5, EPI_BIAS_GELU, 2, 8, 4>(ma, mb4, a, tiles4, st, &md)
+                    : launch_tc<256, 5, EPI_BIAS, 2, 8, 4>(ma, mb4, a, tiles4, st, &md);
+      int r2 = gelu ? launch_tc<256, 5, EPI_BIAS_GELU, 2, 8, 2, 2>(ma, mb, a, tiles4, side, &md,
+                                                                     left - left % 2)
+                    : launch_tc<256, 5, EPI_BIAS, 2, 8, 2, 2>(ma, mb, a, tiles4, side, &md,
+                                                             left - left % 2);
+      cudaEventRecord(join, side);
+      cudaStreamWaitEvent(st, join, 0);
+      return r1 ? r1 : r2;
+    }
+    if (cluster4 == 1 && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
         (N % 8) == 0 && a_gather == nullptr && make_map_out3d(&md, D, G, per_group, N) == 0) {
       // two CTA pairs per cluster (m-blocks 2j, 2j+1) sharing the weight tile by multicast
       CUtensorMap mb4;
