@@ -49,6 +49,25 @@ def test_invalid_arguments_rejected_without_launch():
                                   None) == _lib.MOE_EINVAL
     assert lib.moe_grouped_gemm_bf16(None, 8, 12, None, 8, 8, None, None, 1, None, 0, None, 8,
                                       None, 8, 0, None) == _lib.MOE_EINVAL
+    # newer entry points: shape / flag checks come before any device work
+    assert lib.moe_grouped_gemm_bf16_wgrad(None, 8, 12, None, 16, 1, 8, None, 8, None,
+                                           None) == _lib.MOE_EINVAL          # P % 8
+    assert lib.moe_gemm_bf16_wgrad_f32(None, 8, 16, None, 10, None, None) == _lib.MOE_EINVAL
+    assert lib.moe_colsum_rows_bf16(None, 12, 1, 0, None, 8, None, None) == _lib.MOE_EINVAL
+    assert lib.moe_gather_rows(None, 24, None, 4, None, None) == _lib.MOE_EINVAL  # row_bytes % 16
+    assert lib.moe_grouped_gemm_bf16_gather(None, 8, None, 64, None, 64, 64, None, None, 1, 0,
+                                            None, 8, 8, 0, None) == _lib.MOE_EINVAL  # row_stride 0
+    assert lib.moe_grouped_gemm_bf16(None, 8, 64, None, 8, 8, None, None, 1, None, 0, None, 8,
+                                      None, 8, 2 | _lib.MOE_GEMM_PAD_SCRATCH,
+                                      None) == _lib.MOE_EINVAL      # act 2 is not a plain GEMM
+    assert lib.moe_ep_plan_chunked(None, 4, 0, 6, 1, 8, None, None, None, None, None,
+                                   None) == _lib.MOE_EINVAL         # E % world
+    assert lib.moe_ep_plan_chunked(None, 2, 0, 8, 0, 8, None, None, None, None, None,
+                                   None) == _lib.MOE_EINVAL         # chunks >= 1
+    assert lib.moe_set_launch_limits(-1, 0) == _lib.MOE_EINVAL
+    assert lib.moe_set_launch_limits(0, 0) == 0
+    assert lib.moe_gate_bwd(None, 4, 8, 4, 1, None, None, None, None, 0,
+                            None) == _lib.MOE_EINVAL                # Epad < E
     # empty work is a no-op success
     assert lib.moe_topk_gate(None, 0, 0, 8, 1, None, None, None, None) == 0
     assert lib.moe_exclusive_scan_i64(None, 0, None, None, 0, None) == 0
