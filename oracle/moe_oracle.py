@@ -197,6 +197,25 @@ def sparse_dispatch_oracle(batch, expert_ids, num_experts, cap):
     return np.einsum("sec,sm->ecm", mask, np.asarray(batch, dtype=np.float64))
 
 
+def sparse_combine_oracle(outputs, expert_ids, gate_probs, num_experts, cap):
+    """Gate-prob weighted one-hot contraction back to tokens (gating.py:351-377):
+    every kept assignment (t, j) contributes p[t, j] * outputs[e, slot]; the
+    weight tensor is the dispatch mask with each assignment's ones scaled by
+    its gate prob, contracted as einsum("sec,ecm->sm")."""
+    expert_ids = np.asarray(expert_ids)
+    s, k = expert_ids.shape
+    flat = expert_ids.reshape(-1)
+    hot = flat[:, None] == np.arange(num_experts)[None, :]
+    running = np.cumsum(hot, axis=0) - hot
+    wmask = np.zeros((s * k, num_experts, cap))
+    r, c = np.where(hot)
+    sl = running[r, c]
+    ok = sl < cap
+    wmask[r[ok], c[ok], sl[ok]] = np.asarray(gate_probs, dtype=np.float64).reshape(-1)[r[ok]]
+    w = wmask.reshape(s, k, num_experts, cap).sum(axis=1)
+    return np.einsum("sec,ecm->sm", w, np.asarray(outputs, dtype=np.float64))
+
+
 # ---------------------------------------------------------------------------
 # layer
 # ---------------------------------------------------------------------------

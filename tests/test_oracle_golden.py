@@ -73,8 +73,11 @@ def test_scatter_combine():
         assert np.array_equal(occ, z[f"s{i}_occ"])
         comb = O.combine_tokens(np.tanh(data), z[f"s{i}_ids"], z[f"s{i}_slots"], z[f"s{i}_gp"])
         assert np.array_equal(comb, z[f"s{i}_comb"])
-        # one-hot oracle agrees bitwise with the table path (test_gating.py:292-298)
+        # one-hot oracles agree with the table path (test_gating.py:292-308): dispatch
+        # bitwise, combine within 1e-12
         assert np.array_equal(O.sparse_dispatch_oracle(z[f"s{i}_x"], z[f"s{i}_ids"], e, cap), data)
+        oc = O.sparse_combine_oracle(np.tanh(data), z[f"s{i}_ids"], z[f"s{i}_gp"], e, cap)
+        assert np.max(np.abs(oc - z[f"s{i}_comb"]), initial=0.0) <= 1e-12
 
 
 def _layer_case(z, i):
