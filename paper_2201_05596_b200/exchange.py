@@ -37,7 +37,8 @@ import torch.distributed as dist
 
 from . import _lib
 
-__all__ = ["ScheduleError", "ReplicaMismatchError", "ExchangeStats", "Exchanger"]
+__all__ = ["ScheduleError", "ReplicaMismatchError", "ExchangeStats", "Exchanger",
+           "hierarchical_plan", "coordinated_plan"]
 
 
 class ScheduleError(ValueError):
@@ -105,6 +106,67 @@ def _a2a(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group) -> 
     dist.all_to_all_single(out[:n_out], inp[:n_in], output_split_sizes=[int(v) for v in out_splits],
                            input_split_sizes=[int(v) for v in in_splits], group=group)
     return out[:n_out]
+
+
+def hierarchical_plan(C, G: int, r: int) -> dict:
+    """Rank r's side of the two-phase schedule (pure index arithmetic).
+
+    C[s][d]: rows s sends to d, ranks node-major in nodes of G. Phase 1 sends
+    ``inp[idx1]`` split ``in1`` to the node's local ids and receives ``out1``
+    from them ([source local id][destination node] blocks); phase 2 sends
+    ``mid[idx2]`` split ``in2`` along the rail (destination nodes) and receives
+    ``out2``, ordered by global source rank."""
+    C = np.asarray(C, dtype=np.int64)
+    world = C.shape[0]
+    nodes = world // G
+    n, l = divmod(r, G)
+    off = _excl(C[r])
+    d_order = np.array([m * G + lp for lp in range(G) for m in range(nodes)], dtype=np.int64)
+    idx1 = _ranges(off[d_order], C[r][d_order])
+    in1 = [int(C[r][lp::G].sum()) for lp in range(G)]
+    out1 = [int(C[n * G + sp][l::G].sum()) for sp in range(G)]
+    blk = np.array([[C[n * G + sp][m * G + l] for m in range(nodes)] for sp in range(G)],
+                   dtype=np.int64).reshape(G, nodes)
+    boff = _excl(blk.reshape(-1)).reshape(G, nodes)
+    idx2 = _ranges(boff.T.reshape(-1), blk.T.reshape(-1))
+    in2 = [int(blk[:, m].sum()) for m in range(nodes)]
+    out2 = [int(C[mp * G:(mp + 1) * G, r].sum()) for mp in range(nodes)]
+    return dict(idx1=idx1, in1=in1, out1=out1, idx2=idx2, in2=in2, out2=out2)
+
+
+def coordinated_plan(Cg, L: int, rank: int) -> dict:
+    """Rank's side of the coordinated schedule (pure index arithmetic).
+
+    Cg[q][D]: logical rows group q sends to group D. The rail exchange sends
+    ``inp[idx1]`` (positions = t mod L of each destination block) split
+    ``in1`` and receives ``out1`` into a buffer of ``maxh`` rows; after the
+    all-gather inside the group (L x maxh rows, member-major) the group's
+    receive list is ``gathered[idx2]``."""
+    Cg = np.asarray(Cg, dtype=np.int64)
+    Q = Cg.shape[0]
+    q, t = divmod(rank, L)
+
+    def share(c, u):  # rows i < c with i = u (mod L)
+        return np.maximum(0, (np.asarray(c, dtype=np.int64) - u + L - 1) // L)
+
+    off = _excl(Cg[q])
+    cnt = share(Cg[q], t)
+    idx1 = _ranges(off + t, cnt)
+    if L > 1 and idx1.size:  # positions t + L*j inside each block
+        base = np.repeat(off + t, cnt)
+        idx1 = base + (idx1 - base) * L
+    hu = np.stack([share(Cg[:, q], u) for u in range(L)]).reshape(L, Q)  # rows per member
+    maxh = max(int(hu.sum(axis=1).max()), 1)
+    huo = _excl(hu, axis=1)
+    parts = []
+    for qs in range(Q):
+        i = np.arange(int(Cg[qs, q]), dtype=np.int64)
+        u = i % L
+        parts.append(u * maxh + huo[u, qs] + i // L)
+    idx2 = np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
+    held = np.array([[int(share(Cg[:, qq], u).sum()) for u in range(L)] for qq in range(Q)])
+    return dict(idx1=idx1, in1=[int(v) for v in cnt], out1=[int(v) for v in share(Cg[:, q], t)],
+                maxh=maxh, idx2=idx2, allgather_rows=int(held.sum()) * (L - 1))
 
 
 class Exchanger:
@@ -177,23 +239,12 @@ class Exchanger:
                                             payload)
             return _a2a(out, inp, C[:, r], C[r], self.group)
         G, nodes = self.G, self.nodes
-        n, l = divmod(r, G)
-        # layout transform 1: my rows regrouped (destination local id l', node m)
-        off = _excl(C[r])
-        d_order = np.array([m * G + lp for lp in range(G) for m in range(nodes)])
-        send1 = _gather(self._buf("send1", int(C[r].sum()), inp), inp,
-                        _ranges(off[d_order], C[r][d_order]))
-        in1 = [int(sum(C[r][m * G + lp] for m in range(nodes))) for lp in range(G)]
-        out1 = [int(sum(C[n * G + sp][m * G + l] for m in range(nodes))) for sp in range(G)]
-        mid = _a2a(self._buf("mid", sum(out1), inp), send1, out1, in1, self.node_group)
-        # mid = [source local id s'][destination node m] blocks of C[n*G+s'][m*G+l];
-        # layout transform 2: regroup by destination node m
-        blk = np.array([[C[n * G + sp][m * G + l] for m in range(nodes)] for sp in range(G)])
-        boff = _excl(blk.reshape(-1)).reshape(G, nodes)
-        send2 = _gather(self._buf("send2", int(blk.sum()), inp), mid,
-                        _ranges(boff.T.reshape(-1), blk.T.reshape(-1)))
-        in2 = [int(blk[:, m].sum()) for m in range(nodes)]
-        out2 = [int(sum(C[mp * G + sp][r] for sp in range(G))) for mp in range(nodes)]
+        pl = hierarchical_plan(C, G, r)
+        send1 = _gather(self._buf("send1", int(C[r].sum()), inp), inp, pl["idx1"])
+        mid = _a2a(self._buf("mid", sum(pl["out1"]), inp), send1, pl["out1"], pl["in1"],
+                   self.node_group)
+        send2 = _gather(self._buf("send2", pl["idx2"].size, inp), mid, pl["idx2"])
+        out2, in2 = pl["out2"], pl["in2"]
         # received: [source node m'][source local id s'] = ordered by global source rank
         res = _a2a(out, send2, out2, in2, self.rail_group)
         self.last_stats = ExchangeStats("hierarchical", self.world, G + nodes, 0, 2 * payload,
@@ -211,28 +262,14 @@ class Exchanger:
         L, Q = self.L, self.Q
         if Cg.shape != (Q, Q):
             raise ScheduleError(f"group counts shape {Cg.shape} != ({Q}, {Q})")
-        q, t = divmod(self.rank, L)
         row_bytes = int(inp.shape[1] * inp.element_size())
-
-        def share(c, u):  # rows i < c with i = u (mod L)
-            return np.maximum(0, (np.asarray(c, dtype=np.int64) - u + L - 1) // L)
-
-        # layout transform: my share (positions t, t+L, ...) of every destination block
-        off = _excl(Cg[q])
-        cnt = share(Cg[q], t)
-        idx = _ranges(off + t, cnt)
-        if L > 1 and idx.size:
-            # positions t + L*j inside each block: stretch the unit-stride ranges
-            base = np.repeat(off + t, cnt)
-            idx = base + (idx - base) * L
-        send1 = _gather(self._buf("send1", int(cnt.sum()), inp), inp, idx)
-        out1 = share(Cg[:, q], t)
+        pl = coordinated_plan(Cg, L, self.rank)
+        send1 = _gather(self._buf("send1", pl["idx1"].size, inp), inp, pl["idx1"])
         # the rail exchange lands in a buffer padded to the largest member's share,
         # which is then all-gathered inside the tensor group
-        hu = np.stack([share(Cg[:, q], u) for u in range(L)])  # (L, Q) rows per member
-        maxh = max(int(hu.sum(axis=1).max()), 1)
+        maxh = pl["maxh"]
         pad = self._buf("pad", maxh, inp)
-        _a2a(pad, send1, out1, cnt, self.rail_group)
+        _a2a(pad, send1, pl["out1"], pl["in1"], self.rail_group)
         gbuf = self._buf("gath", L * maxh, inp)[:L * maxh]
         if L > 1:
             if dist.get_backend(self.slice_group) == "nccl":
@@ -243,18 +280,10 @@ class Exchanger:
         else:
             gbuf = pad[:maxh]
         # reassemble each source block: position i came from member i % L
-        huo = _excl(hu, axis=1)  # (L, Q) block offsets inside each member's share
-        parts = []
-        for qs in range(Q):
-            i = np.arange(int(Cg[qs, q]), dtype=np.int64)
-            u = i % L
-            parts.append(u * maxh + huo[u, qs] + i // L)
-        idx2 = np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
-        res = _gather(out, gbuf, idx2)
+        res = _gather(out, gbuf, pl["idx2"])
         payload = int(Cg.sum()) * row_bytes
         # all-gather volume: each member's share to its L-1 peers (commsim.py:440-455)
-        held_all = np.array([[int(share(Cg[:, qq], u).sum()) for u in range(L)] for qq in range(Q)])
-        ag = int(held_all.sum()) * (L - 1) * row_bytes
+        ag = pl["allgather_rows"] * row_bytes
         self.last_stats = ExchangeStats("coordinated", self.world, Q, L, payload + ag, payload,
                                         payload)
         return res

@@ -113,3 +113,97 @@ def test_schedules_match_reference_commsim(world):
 def test_schedule_validation():
     with pytest.raises(ScheduleError):  # checked before any process-group call
         Exchanger(schedule="ring")
+
+
+# ---------------------------------------------------------------------------
+# C6 at scale: the schedules' index plans, with the collectives simulated in
+# NumPy, for every world size 1..64 and every node size / tensor slice that
+# divides it (pkg/tests/test_acceptance.py::test_c06_schedule_equivalence)
+# ---------------------------------------------------------------------------
+
+def _payload(world, per_rank, seed):
+    """synthetic_sends-like payload: per rank, items with random destinations;
+    rows tagged (src, token), each rank's rows ordered by destination."""
+    rng = np.random.default_rng(seed)
+    C = np.zeros((world, world), dtype=np.int64)
+    rows, token = [], 0
+    for src in range(world):
+        dst = rng.integers(world, size=per_rank)
+        toks = np.arange(token, token + per_rank)
+        token += per_rank
+        order = np.argsort(dst, kind="stable")
+        rows.append(np.stack([np.full(per_rank, src), toks[order]], axis=1))
+        np.add.at(C[src], dst, 1)
+    return C, rows
+
+
+def _split(a, sizes):
+    return np.split(a, np.cumsum(sizes)[:-1]) if len(sizes) else []
+
+
+def _flat(C, rows):
+    world = len(rows)
+    chunks = [_split(rows[s], C[s]) for s in range(world)]
+    return [np.concatenate([chunks[s][d] for s in range(world)]) for d in range(world)]
+
+
+def _sim_hier(C, rows, G):
+    from paper_2201_05596_b200.exchange import hierarchical_plan
+
+    world, nodes = len(rows), len(rows) // G
+    pl = [hierarchical_plan(C, G, r) for r in range(world)]
+    send1 = [_split(rows[r][pl[r]["idx1"]], pl[r]["in1"]) for r in range(world)]
+    mid = []
+    for r in range(world):
+        n, l = divmod(r, G)
+        m_ = np.concatenate([send1[n * G + sp][l] for sp in range(G)])
+        assert len(m_) == sum(pl[r]["out1"])
+        mid.append(m_)
+    send2 = [_split(mid[r][pl[r]["idx2"]], pl[r]["in2"]) for r in range(world)]
+    out = []
+    for r in range(world):
+        m, l = divmod(r, G)
+        o = np.concatenate([send2[mp * G + l][m] for mp in range(nodes)])
+        assert len(o) == sum(pl[r]["out2"])
+        out.append(o)
+    return out
+
+
+def _sim_coord(Cg, rows_g, L):
+    from paper_2201_05596_b200.exchange import coordinated_plan
+
+    Q = len(rows_g)
+    world = Q * L
+    pl = [coordinated_plan(Cg, L, r) for r in range(world)]
+    send1 = [_split(rows_g[r // L][pl[r]["idx1"]], pl[r]["in1"]) for r in range(world)]
+    held = []
+    for r in range(world):
+        q, t = divmod(r, L)
+        h = np.concatenate([send1[d * L + t][q] for d in range(Q)])  # rail t, from every group
+        assert len(h) == sum(pl[r]["out1"])
+        pad = np.full((pl[r]["maxh"], 2), -1, dtype=np.int64)
+        pad[:len(h)] = h
+        held.append(pad)
+    out = []
+    for r in range(world):
+        q = r // L
+        gathered = np.concatenate([held[q * L + u] for u in range(L)])  # all-gather in the group
+        out.append(gathered[pl[r]["idx2"]])
+    return out
+
+
+def test_c06_schedule_plans_at_scale():
+    for p in range(1, 65):
+        C, rows = _payload(p, 3, seed=p)
+        flat = _flat(C, rows)
+        divisors = [d for d in range(1, p + 1) if p % d == 0]
+        for G in divisors:
+            hier = _sim_hier(C, rows, G)
+            for r in range(p):
+                assert np.array_equal(hier[r], flat[r]), (p, G, r)
+        for L in divisors:
+            Cg, rows_g = _payload(p // L, 3, seed=1000 + p)
+            base = _flat(Cg, rows_g)
+            coord = _sim_coord(Cg, rows_g, L)
+            for r in range(p):
+                assert np.array_equal(coord[r], base[r // L]), (p, L, r)
