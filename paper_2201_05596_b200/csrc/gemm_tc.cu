@@ -1115,25 +1115,34 @@ static int* dyn_counter(cudaStream_t st, int64_t K = 0, int64_t N = 0, bool forc
     return v ? atoi(v) : 2;
   }();
   if (!force && (!enabled || (enabled == 2 && K < 2 * N))) return nullptr;
+  // slots [0, kPool) rotate for eager launches; launches captured into CUDA graphs
+  // take slots from [kPool, 2*kPool) that are never handed out again (a replayed
+  // graph re-zeroes and reuses its own slot), static schedule once those run out
   constexpr int kPool = 4096;
   static int* pool[64] = {};
-  static unsigned next[64] = {};
+  static unsigned next[64] = {}, next_graph[64] = {};
   static std::mutex mu;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
   int* c = nullptr;
   {
     std::lock_guard<std::mutex> lock(mu);
     if (pool[dev] == nullptr) {
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(st, &cs);
-      if (cs != cudaStreamCaptureStatusNone) return nullptr;  // no allocation inside a capture
-      if (cudaMalloc(&pool[dev], kPool * sizeof(int)) != cudaSuccess) {
+      if (capturing) return nullptr;  // no allocation inside a capture
+      if (cudaMalloc(&pool[dev], 2 * kPool * sizeof(int)) != cudaSuccess) {
         pool[dev] = nullptr;
         return nullptr;
       }
     }
-    c = pool[dev] + (next[dev]++ % kPool);
+    if (capturing) {
+      if (next_graph[dev] >= (unsigned)kPool) return nullptr;
+      c = pool[dev] + kPool + next_graph[dev]++;
+    } else {
+      c = pool[dev] + (next[dev]++ % kPool);
+    }
   }
   if (cudaMemsetAsync(c, 0, sizeof(int), st) != cudaSuccess) return nullptr;
   return c;
