@@ -186,14 +186,17 @@ int moe_grouped_gemm_bf16_gather(const void* X, int64_t x_rows, const int32_t* r
  * epilogue (gating.py:281-307, arch.py:389): for every expert-buffer row r
  *   out[row_token[r]] = x_resid[row_token[r]] + row_prob[r] * (A[r] @ B_w^T + bias_w)
  * row_token / row_prob come from moe_dispatch_fused, which also writes
- * out[t] = x[t] for fully dropped tokens. Other arguments as above. */
+ * out[t] = x[t] for fully dropped tokens. y_out (nullable, (a_rows, N) bf16)
+ * additionally keeps the expert outputs A[r] @ B_w^T + bias_w per row (the
+ * training forward needs them for the gate-probability gradient). Other
+ * arguments as above. */
 int moe_grouped_gemm_bf16_combine(const void* A, int64_t a_rows, int K, const void* B,
                                   int64_t b_rows, int N, const float* bias, int num_groups,
                                   const int32_t* row_start, int64_t row_stride,
                                   const int32_t* rows, int64_t rows_const,
                                   const int32_t* weight_idx, int64_t max_group_rows,
                                   const int32_t* row_token, const float* row_prob,
-                                  const void* x_resid, void* out, void* stream);
+                                  const void* x_resid, void* out, void* y_out, void* stream);
 
 /* fp32 SIMT variant (parity path). B f32 in the reference layout: weight w is
  * (K, N) row-major at B + w*K*N. */

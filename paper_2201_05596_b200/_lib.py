@@ -54,7 +54,7 @@ SIGNATURES = {
     "moe_grouped_gemm_bf16": (_I, [_P, _L, _I, _P, _L, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L,
                                    _I, _P]),
     "moe_grouped_gemm_bf16_combine": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _L, _P, _L, _P,
-                                           _L, _P, _P, _P, _P, _P]),
+                                           _L, _P, _P, _P, _P, _P, _P]),
     "moe_ipc_malloc": (_I, [_Z, _P]),
     "moe_ipc_free": (_I, [_P]),
     "moe_ipc_get_handle": (_I, [_P, _P]),

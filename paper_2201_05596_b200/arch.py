@@ -423,7 +423,7 @@ class MoeLayer:
                 _lib.call("moe_grouped_gemm_bf16_combine", ws["h"].data_ptr(), E * cap, F,
                           self.w2.data_ptr(), E * M, M, self.b2.data_ptr(), E, None, cap,
                           ws["load"].data_ptr(), 0, None, cap, ws["row_token"].data_ptr(),
-                          ws["row_prob"].data_ptr(), x.data_ptr(), out.data_ptr(), st)
+                          ws["row_prob"].data_ptr(), x.data_ptr(), out.data_ptr(), None, st)
             ph(None)
             return out
         _lib.call("moe_dispatch", x.data_ptr(), S, M * x.element_size(), E, k, cap, ids.data_ptr(),

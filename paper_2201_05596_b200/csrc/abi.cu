@@ -253,12 +253,12 @@ int moe_grouped_gemm_bf16_combine(const void* A, int64_t a_rows, int K, const vo
                                   const int32_t* rows, int64_t rows_const,
                                   const int32_t* weight_idx, int64_t max_group_rows,
                                   const int32_t* row_token, const float* row_prob,
-                                  const void* x_resid, void* out, void* stream) {
+                                  const void* x_resid, void* out, void* y_out, void* stream) {
   CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1);
   CHECK(max_group_rows >= 0 && rows_const >= 0);
   if (a_rows == 0 || max_group_rows == 0) return MOE_OK;
   CHECK(A && B && row_token && row_prob && x_resid && out);
-  return moe::launch_grouped_gemm_bf16(A, a_rows, K, B, b_rows, N, bias, nullptr, num_groups,
+  return moe::launch_grouped_gemm_bf16(A, a_rows, K, B, b_rows, N, bias, y_out, num_groups,
                                        row_start, row_stride, rows, rows_const, weight_idx,
                                        max_group_rows, 2, S_(stream), row_token, row_prob,
                                        x_resid, out);

@@ -788,6 +788,25 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             }
           }
           if constexpr (EPI == EPI_BIAS_COMBINE) {
+            if (args.D != nullptr) {  // training: also keep y = acc + b2 (row layout) for backward
+              __nv_bfloat16* yrow = args.D + out_row * N;
+              if (vec_ok && col0 + 32 <= N) {
+                uint4* yd = reinterpret_cast<uint4*>(yrow + col0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  uint4 pk;
+                  pk.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                  pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                  pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                  pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                  yd[q] = pk;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (col0 + i < N) yrow[col0 + i] = __float2bfloat16_rn(v[i]);
+              }
+            }
             if (vec_ok && col0 + 32 <= N) {
               const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(xbuf[c & 1]);
 #pragma unroll

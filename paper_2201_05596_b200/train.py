@@ -100,6 +100,24 @@ def forward_train(layer, x: torch.Tensor) -> torch.Tensor:
                   st)
         _lib.call("moe_plan_scan", tc.data_ptr(), S, E, cap, None, ws["tile_offsets"].data_ptr(),
                   ws["totals"].data_ptr(), load.data_ptr(), st)
+    # k=1 without a shared MLP: combine + residual fused into GEMM2's epilogue, which
+    # also keeps y (the gate-probability gradient needs it); otherwise a separate combine
+    fused = k == 1 and layer.shared is None
+    if S and fused:
+        i32 = dict(dtype=torch.int32, device=dev)
+        row_token = torch.empty(max(E * cap, 1), **i32)
+        row_prob = torch.empty(max(E * cap, 1), dtype=torch.float32, device=dev)
+        _lib.call("moe_dispatch_fused", x.data_ptr(), S, M * 2, E, k, cap, ids.data_ptr(),
+                  lr.data_ptr(), ws["tile_offsets"].data_ptr(), gp.data_ptr(), slots.data_ptr(),
+                  xbuf.data_ptr(), row_token.data_ptr(), row_prob.data_ptr(), out.data_ptr(), st)
+        if cap:
+            _gemm(xbuf, E * cap, M, layer.w1, F, layer.b1, h, E, cap, load, 0, cap,
+                  _lib.MOE_ACT_GELU_SAVE, a)
+            _lib.call("moe_grouped_gemm_bf16_combine", h.data_ptr(), E * cap, F,
+                      layer.w2.data_ptr(), E * M, M, layer.b2.data_ptr(), E, None, cap,
+                      load.data_ptr(), 0, None, cap, row_token.data_ptr(), row_prob.data_ptr(),
+                      x.data_ptr(), out.data_ptr(), y.data_ptr(), st)
+    elif S:
         _lib.call("moe_dispatch", x.data_ptr(), S, M * 2, E, k, cap, ids.data_ptr(),
                   lr.data_ptr(), ws["tile_offsets"].data_ptr(), slots.data_ptr(),
                   xbuf.data_ptr(), st)
@@ -117,7 +135,7 @@ def forward_train(layer, x: torch.Tensor) -> torch.Tensor:
         _gemm(x, S, M, s.w1, F, s.b1, h_s, 1, 0, None, S, S, _lib.MOE_ACT_GELU_SAVE, a_s)
         _gemm(h_s, S, F, s.w2, M, s.b2, shared_out, 1, 0, None, S, S)
         sh_ctx = (a_s, h_s)
-    if S:
+    if S and not fused:
         _lib.call("moe_combine", y.data_ptr(), _lib.MOE_BF16, S, M, E, k, cap, ids.data_ptr(),
                   slots.data_ptr(), None, gp.data_ptr(), _lib.MOE_F32, x.data_ptr(),
                   _lib.ptr(shared_out), out.data_ptr(), 1, st)
