@@ -32,7 +32,11 @@ class HostPipeline:
     def _alloc(self, rows: int) -> None:
         if rows == self.rows:
             return
+        # the old slots may still be read by an in-flight copy on either copy stream
+        # (the caching allocator would hand them out again to this stream at once)
         torch.cuda.current_stream(self.device).synchronize()
+        self.h2d.synchronize()
+        self.d2h.synchronize()
         self.x_dev = [torch.empty((rows, self.width), dtype=self.dtype, device=self.device)
                       for _ in range(2)]
         self.y_dev = [torch.empty((rows, self.width), dtype=self.dtype, device=self.device)
