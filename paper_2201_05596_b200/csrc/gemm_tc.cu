@@ -120,7 +120,7 @@ struct Smem {
   static constexpr int kBarOff = STAGES * kStageBytes;
   // full/empty ring, 2 x tfull/tempty, tmem slot, pbar ring, tile-queue full/empty
   // barriers and the tile-queue slots (dynamic scheduling)
-  static constexpr int kBarBytes = (3 * STAGES + 4 + 2 * kTileQ) * 8 + 16 + kTileQ * 4;
+  static constexpr int kBarBytes = (3 * STAGES + 8 + 2 * kTileQ) * 8 + 16 + kTileQ * 4;
   static constexpr int kTileOff = kBarOff + kBarBytes;
   static constexpr int kBiasOff = (kTileOff + (kMaxGroups + 1) * 4 + 127) / 128 * 128;  // AS x BN fp32
   // epilogue staging for TMA stores: OUT bytes, 1024-aligned
@@ -172,6 +172,13 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   // each CTA holding 128 B rows of each (two 16 KB halves of its B stage)
   constexpr int kNI = (CG == 2 && BN > 256) ? BN / 256 : 1;
   static_assert(kNI == 1 || (CG == 2 && BN == 512), "BN = 512 needs the 2-CTA pair");
+  // BN = 512 forward tiles hand the accumulator over in kParts column parts of
+  // kPW (tfull/tempty[j]; N = kPW MMAs) so the epilogue overlaps the MMAs
+  // without a second accumulator buffer
+  constexpr bool kSplit = kNI == 2 && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_COMBINE);
+  // (two N=256 halves: N=128 parts re-read A from smem twice as often and measured slower)
+  constexpr int kParts = kSplit ? 2 : 1;
+  constexpr int kPW = BN / kParts;
   constexpr bool kMN = EPI == EPI_WGRAD || EPI == EPI_WGRAD_ACC;  // MN-major operands
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -179,9 +186,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint64_t* pbar = tempty + 3;  // [STAGES] weight-gradient partial K blocks (CTA-local)
+  uint64_t* tempty = tfull + 4;  // [4]: accumulator stages, or the kSplit column parts
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+  uint64_t* pbar = tempty + 5;  // [STAGES] weight-gradient partial K blocks (CTA-local)
   uint64_t* tq_full = pbar + STAGES;   // [kTileQ]
   uint64_t* tq_empty = tq_full + kTileQ;
   volatile int* tq = reinterpret_cast<volatile int*>(tq_empty + kTileQ);
@@ -231,7 +238,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         mbar_init(&full[s], CG);  // CG=2: the peer's producer arrives remotely on the leader's
         mbar_init(&empty[s], CLP);  // CL=4: both pairs' MMAs release every stage
       }
-      for (int a = 0; a < AS; ++a) {
+      for (int a = 0; a < (kSplit ? kParts : AS); ++a) {
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], EW * CG);  // every epilogue warp of the pair arrives
       }
@@ -542,6 +549,66 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         const int64_t kg = args.k_rows ? args.k_rows[g] : args.k_rows_const;
         kb_end = (int)((kg + BK - 1) / BK);  // 0 for an empty group: the epilogue writes zeros
       }
+      if constexpr (kSplit) {
+        // BN = 512 pair tile, TMEM full: the accumulator is handed over in kParts
+        // column parts (MMAs of N = kPW, each CTA holding kPW/2 B rows of a part).
+        // First kRA K blocks: parts 0.. run ahead while the epilogue still drains the
+        // later parts of the previous tile; last kRA K blocks: part by part, so the
+        // epilogue of part j overlaps the tail MMAs of parts j+1...
+        constexpr uint32_t idesc_p = make_idesc_bf16(TM, kPW);
+        const int s0 = stage;
+        const uint32_t ph0 = phase;
+        auto wait_kb = [&](int kb) {
+          mbar_wait(&full[(s0 + kb) % STAGES], ph0 ^ (uint32_t)(((s0 + kb) / STAGES) & 1));
+          tc_fence_after();
+        };
+        auto mma_part = [&](int kb, int j) {
+          if (lane == 0) {
+            const uint8_t* sa = smem + ((s0 + kb) % STAGES) * L::kStageBytes;
+            const uint64_t adesc = make_sdesc_sw128(sa);
+            const uint64_t bdesc =
+                make_sdesc_sw128(sa + L::kABytes) + (uint64_t)j * (((kPW / 2) * BK * 2) >> 4);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_bf16_cg2(tmem_base + j * kPW, adesc + kStep * kk, bdesc + kStep * kk, idesc_p,
+                            (kb | kk) != 0);
+          }
+        };
+        auto release = [&](int kb) {
+          if (lane == 0) umma_commit_cg2(&empty[(s0 + kb) % STAGES], CL == 4 ? 0xF : 0x3);
+        };
+        constexpr int kRA = STAGES - 1;
+        const int ra = kb_end < kRA ? kb_end : kRA;
+        const int c0 = kb_end - kRA > ra ? kb_end - kRA : ra;
+        for (int j = 0; j < kParts; ++j) {
+          mbar_wait(&tempty[j], acc_phase ^ 1);
+          tc_fence_after();
+          for (int kb = 0; kb < ra; ++kb) {
+            if (j == 0) wait_kb(kb);
+            mma_part(kb, j);
+            if (j == kParts - 1) release(kb);
+          }
+        }
+        for (int kb = ra; kb < c0; ++kb) {
+          wait_kb(kb);
+#pragma unroll
+          for (int j = 0; j < kParts; ++j) mma_part(kb, j);
+          release(kb);
+        }
+        for (int j = 0; j < kParts; ++j) {
+          for (int kb = c0; kb < kb_end; ++kb) {
+            if (j == 0) wait_kb(kb);
+            mma_part(kb, j);
+            if (j == kParts - 1) release(kb);
+          }
+          if (lane == 0) umma_commit_cg2(&tfull[j], (uint16_t)(0x3u << pl));
+        }
+        __syncwarp();
+        stage = (s0 + kb_end) % STAGES;
+        phase = ph0 ^ (uint32_t)(((s0 + kb_end) / STAGES) & 1);
+        acc_phase ^= 1;
+        continue;
+      }
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -628,8 +695,22 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       bool kzero = false;  // weight gradient of a group with no rows: zeros, TMEM not written
       if constexpr (kMN) kzero = (args.k_rows ? args.k_rows[g] : args.k_rows_const) == 0;
 
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait(&tfull[kSplit ? 0 : acc], acc_phase);
       tc_fence_after();
+      // TMEM column and tile column of this warp's 32-column chunk c. kSplit: chunks
+      // 2j, 2j+1 lie in column part j (handed over separately); part j's first
+      // kPW/2 columns come from the leader's B rows, the rest from the peer's
+      // (B rows of half h = j/2 map to tile columns h*256 + cta*128 + ...)
+      constexpr int kCP = kChunks / kParts;  // chunks per part per warp
+      auto tmem_col = [&](int c) -> int {
+        return kSplit ? (c / kCP) * kPW + col_part * (kPW / 2) + (c % kCP) * 32
+                      : (col_part * kChunks + c) * 32;
+      };
+      auto chunk_col = [&](int c) -> int {
+        const int rr = (c / kCP) * (kPW / 2) + (c % kCP) * 32;  // B row in CTA col_part
+        return kSplit ? (rr / 128) * 256 + col_part * 128 + rr % 128 : (col_part * kChunks + c) * 32;
+      };
+      const uint32_t t_lane = tmem_base + ((quarter * 32) << 16) + acc * BN;
       const uint32_t t_addr = tmem_base + ((quarter * 32) << 16) + acc * BN +
                               (EPI != EPI_GATE ? col_part * kChunks * 32 : 0);
 
@@ -661,7 +742,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         constexpr bool kLoadX = EPI == EPI_BIAS_COMBINE || EPI == EPI_GELU_BWD;
         // residual row chunks (COMBINE) are prefetched one chunk ahead
         auto load_x = [&](int c, uint4 (&xq)[4]) {
-          const int col0 = nb * BN + (col_part * kChunks + c) * 32;
+          const int col0 = nb * BN + chunk_col(c);
           if (valid && vec_ok && col0 + 32 <= N) {
             const uint4* xs = reinterpret_cast<const uint4*>(xrow + col0);
 #pragma unroll
@@ -674,16 +755,26 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         // TMEM loads double-buffered across 32-column chunks: the load of
         // chunk c+1 is in flight while chunk c is biased, activated and stored.
         uint32_t r[2][32];
-        tmem_ld_32x32b_x32(t_addr, r[0]);
+        tmem_ld_32x32b_x32(t_lane + tmem_col(0), r[0]);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
-          const int cl = (col_part * kChunks + c) * 32;  // column inside the tile
+          const int cl = chunk_col(c);  // column inside the tile
           const int col0 = nb * BN + cl;
           if constexpr (kLoadX) {
             if (c + 1 < kChunks) load_x(c + 1, xbuf[(c + 1) & 1]);
           }
           tmem_ld_wait_regs(r[c & 1]);
-          if (c + 1 < kChunks) tmem_ld_32x32b_x32(t_addr + (c + 1) * 32, r[(c + 1) & 1]);
+          if constexpr (kSplit) {
+            if (c % kCP == kCP - 1 && c + 1 < kChunks) {
+              // part c/kCP read out: hand it back to the MMA, then wait for the next part
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster(&tempty[c / kCP], pl);
+              mbar_wait(&tfull[c / kCP + 1], acc_phase);
+              tc_fence_after();
+            }
+          }
+          if (c + 1 < kChunks) tmem_ld_32x32b_x32(t_lane + tmem_col(c + 1), r[(c + 1) & 1]);
           // whole warp: 32 rows x 32 columns -> smem (row = lane, 64 B, 64-B swizzle)
           // -> one TMA tensor store; rows / columns past the group's block are
           // clipped by the 3-D map (N, rows per group, G)
@@ -851,7 +942,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         __syncwarp();
         if (lane == 0) {
           if constexpr (CG == 2)
-            mbar_arrive_cluster(&tempty[acc], pl);  // the leader's MMA reuses this accumulator
+            mbar_arrive_cluster(&tempty[kSplit ? kParts - 1 : acc], pl);  // the leader's MMA reuses it
           else
             mbar_arrive(&tempty[acc]);
         }
@@ -1350,6 +1441,17 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
     }
   }
   if (act == 2) {  // fused combine epilogue
+    static const int bn512c = [] {
+      const char* v = getenv("MOE_BN512");
+      return v ? atoi(v) : 0;
+    }();
+    if (CG == 2 && bn512c == 1 && (N % 512) == 0) {
+      CUtensorMap mb2;
+      rc = make_map(&mb2, B, b_rows, K, 128);
+      if (rc) return rc;
+      const int64_t tiles512 = (int64_t)G * ((max_group_rows + tm - 1) / tm) * ((N + 511) / 512);
+      return launch_tc<512, 4, EPI_BIAS_COMBINE, 2, 8>(ma, mb2, a, tiles512, st);
+    }
     if (CG == 2) return launch_tc<256, 6, EPI_BIAS_COMBINE, 2, 8>(ma, mb, a, max_tiles, st);
     switch (BN) {
       case 32: return launch_tc<32, 8, EPI_BIAS_COMBINE, 1, 4>(ma, mb, a, max_tiles, st);
@@ -1375,13 +1477,17 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
 #ifndef MOE_FWD_EW
 #define MOE_FWD_EW 8
 #endif
+    // MOE_BN512: 256 x 512 pair tiles (25% less operand traffic per flop) for
+    // 0 none, 1 every eligible forward GEMM, 2 (default) the plain-bias ones: the
+    // GELU epilogue's tanh (MUFU-bound) drains a half slower than the MMAs refill
+    // it, the bias-only epilogue keeps up (C2 / C4 +3-5%, GEMM1 at C3 -2%)
     static const int bn512 = [] {
       const char* v = getenv("MOE_BN512");
-      return v ? atoi(v) : 0;
+      return v ? atoi(v) : 2;
     }();
-    if (bn512 && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
+    if ((bn512 == 1 || (bn512 == 2 && !gelu)) && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
         (N % 512) == 0 && make_map_out3d(&md, D, G, per_group, N) == 0) {
-      // 256 x 512 pair tiles: 25% less operand traffic per flop, no accumulator overlap
+      // 256 x 512 pair tiles; TMEM holds one accumulator, handed over in two halves
       CUtensorMap mb2;
       rc = make_map(&mb2, B, b_rows, K, 128);
       if (rc) return rc;
