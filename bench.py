@@ -18,6 +18,7 @@ forward_layer) on a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -58,7 +59,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--decode-iters", type=int, default=50)
-    ap.add_argument("--train-steps", type=int, default=5)
+    ap.add_argument("--train-steps", type=int, default=10)
     ap.add_argument("--no-decode-graph", dest="decode_graph", action="store_false")
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
                     help="N>1 exchange transport (auto: peer memory for k=1 layers)")
@@ -187,27 +188,36 @@ class Clocks:
         self.p.terminate()
         self.p.wait()
         self.f.flush()
-        rows = []
+        stamped = []
         for line in open(self.f.name):
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
             try:
                 ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
-                if self.t0 is not None and not (self.t0 <= ts <= t1):
-                    continue
-                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+                stamped.append((ts, (float(parts[1]), float(parts[2]), parts[5:9])))
             except ValueError:
                 continue
         os.unlink(self.f.name)
+        t0 = self.t0 if self.t0 is not None else -float("inf")
+        rows = [r for ts, r in stamped if t0 <= ts <= t1]
+        note = None
+        if not rows:
+            # a timed region shorter than nvidia-smi's effective sampling period:
+            # report the samples taken within 250 ms of it
+            rows = [r for ts, r in stamped if t0 - 0.25 <= ts <= t1 + 0.25]
+            note = "no sample inside the timed region; samples within 250 ms of it"
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         mx = max(r[1] for r in rows)
         loaded = [r for r in rows if r[0] > 0.5 * mx] or rows
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[2]) if v == "Active"})
-        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": mx,
-                "reasons": reasons, "samples": len(rows)}
+        out = {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": mx,
+               "reasons": reasons, "samples": len(rows)}
+        if note:
+            out["note"] = note
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -351,20 +361,23 @@ def run_gpu(args):
     train = None
     if world == 1 and args.train_steps > 0 and hasattr(layer, "forward_train"):
         gy = torch.randn(S, M, device=dev, generator=gen).to(torch.bfloat16)
-        for _ in range(2):
+        for _ in range(3):
             layer.forward_train(x)
             layer.backward(gy)
         torch.cuda.synchronize()
-        b0 = torch.cuda.Event(enable_timing=True)
-        b1 = torch.cuda.Event(enable_timing=True)
-        b0.record()
-        for _ in range(args.train_steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.train_steps + 1)]
+        gc.disable()  # no collector pauses between the host-side launches of a step
+        ev[0].record()
+        for i in range(args.train_steps):
             layer.forward_train(x)
             layer.backward(gy)
-        b1.record()
+            ev[i + 1].record()
         torch.cuda.synchronize()
-        tms = b0.elapsed_time(b1) / args.train_steps
-        train = {"ms_per_step": round(tms, 3), "tokens_per_s": S / (tms * 1e-3),
+        gc.enable()
+        per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.train_steps)]
+        tms = ev[0].elapsed_time(ev[-1]) / args.train_steps
+        train = {"ms_per_step": round(tms, 3), "ms_per_step_median": round(statistics.median(per), 3),
+                 "tokens_per_s": S / (tms * 1e-3),
                  "gemm_tflops": 12.0 * kept * M * F / (tms * 1e-3) / 1e12,
                  "steps": args.train_steps, "note": "forward_train + backward, bf16"}
         layer._train_ctx = None
