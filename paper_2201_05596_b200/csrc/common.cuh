@@ -429,6 +429,16 @@ MOE_DEV float gelu_tanh_fast(float x) {
   return fmaf(hx, tanh_fast(inner), hx);
 }
 
+// the same GELU from w = x/2 (the expert GEMM1 epilogue folds the halving into
+// its bias add): x(1+tanh(c x (1 + 0.044715 x^2)))/2 = w + w tanh(w (2c + 8c 0.044715 w^2)),
+// five FP32 operations + one tanh instead of seven
+MOE_DEV float gelu_tanh_fast_half(float w) {
+  const float k0 = 1.5957691216057308f;   // 2c
+  const float k1 = 0.28541926509040100f;  // 8c * 0.044715
+  const float inner = w * fmaf(k1, w * w, k0);
+  return fmaf(w, tanh_fast(inner), w);
+}
+
 // d/dx of the tanh-form GELU (the vjp of tensor.py:229-233)
 MOE_DEV float gelu_tanh_grad_fast(float x) {
   const float c = 0.7978845608028654f;

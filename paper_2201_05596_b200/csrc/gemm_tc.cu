@@ -723,7 +723,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           const float* bias = args.bias ? args.bias + (int64_t)w * N : nullptr;
           for (int i = (warp - 2) * 32 + lane; i < BN; i += EW * 32) {
             const int col = nb * BN + i;
-            sbias[i] = (bias != nullptr && col < N) ? __ldg(bias + col) : 0.f;
+            // EPI_BIAS_GELU stages b/2: its epilogue works on w = (acc + b)/2 (exact)
+            sbias[i] = (bias != nullptr && col < N) ? __ldg(bias + col) * (EPI == EPI_BIAS_GELU ? 0.5f : 1.f)
+                                                    : 0.f;
           }
           named_bar_sync(2, EW * 32);
         }
@@ -817,10 +819,11 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float4 bq = b4[q];
-            v[4 * q + 0] = __uint_as_float(r[c & 1][4 * q + 0]) + bq.x;
-            v[4 * q + 1] = __uint_as_float(r[c & 1][4 * q + 1]) + bq.y;
-            v[4 * q + 2] = __uint_as_float(r[c & 1][4 * q + 2]) + bq.z;
-            v[4 * q + 3] = __uint_as_float(r[c & 1][4 * q + 3]) + bq.w;
+            constexpr float sc = EPI == EPI_BIAS_GELU ? 0.5f : 1.f;
+            v[4 * q + 0] = fmaf(__uint_as_float(r[c & 1][4 * q + 0]), sc, bq.x);
+            v[4 * q + 1] = fmaf(__uint_as_float(r[c & 1][4 * q + 1]), sc, bq.y);
+            v[4 * q + 2] = fmaf(__uint_as_float(r[c & 1][4 * q + 2]), sc, bq.z);
+            v[4 * q + 3] = fmaf(__uint_as_float(r[c & 1][4 * q + 3]), sc, bq.w);
           }
           if constexpr (EPI == EPI_WGRAD_ACC) {  // split-K partial: fp32 reduction in HBM/L2
             if (kzero) continue;
@@ -860,7 +863,11 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
                 if (col0 + i < N) arow[col0 + i] = __float2bfloat16_rn(v[i]);
             }
           }
-          if constexpr (EPI == EPI_BIAS_GELU || EPI == EPI_GELU_SAVE) {
+          if constexpr (EPI == EPI_BIAS_GELU) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = gelu_tanh_fast_half(v[i]);
+          }
+          if constexpr (EPI == EPI_GELU_SAVE) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = gelu_tanh_fast(v[i]);
           }
