@@ -30,6 +30,9 @@ from . import _lib
 
 def _gemm(a, a_rows, K, w, N, bias, d, G, row_stride, rows, rows_const, max_rows, act=0,
           aux=None):
+    """act may carry MOE_GEMM_PAD_SCRATCH: the groups' padding rows of d are never
+    read (combine / dx assembly read kept slots only), so the GEMM may use its
+    TMA-store epilogue and 256x512 tiles."""
     st = _lib.stream_ptr()
     if act in (_lib.MOE_ACT_GELU_SAVE, _lib.MOE_ACT_GELU_BWD):
         _lib.call("moe_grouped_gemm_bf16_aux", a.data_ptr(), a_rows, K, w.data_ptr(), w.shape[0],
@@ -124,7 +127,7 @@ def forward_train(layer, x: torch.Tensor) -> torch.Tensor:
         if cap:
             _gemm(xbuf, E * cap, M, layer.w1, F, layer.b1, h, E, cap, load, 0, cap,
                   _lib.MOE_ACT_GELU_SAVE, a)
-            _gemm(h, E * cap, F, layer.w2, M, layer.b2, y, E, cap, load, 0, cap)
+            _gemm(h, E * cap, F, layer.w2, M, layer.b2, y, E, cap, load, 0, cap, _lib.MOE_GEMM_PAD_SCRATCH)
     sh_ctx = None
     shared_out = None
     if layer.shared is not None and S:
@@ -133,7 +136,7 @@ def forward_train(layer, x: torch.Tensor) -> torch.Tensor:
         h_s = torch.empty_like(a_s)
         shared_out = torch.empty_like(x)
         _gemm(x, S, M, s.w1, F, s.b1, h_s, 1, 0, None, S, S, _lib.MOE_ACT_GELU_SAVE, a_s)
-        _gemm(h_s, S, F, s.w2, M, s.b2, shared_out, 1, 0, None, S, S)
+        _gemm(h_s, S, F, s.w2, M, s.b2, shared_out, 1, 0, None, S, S, _lib.MOE_GEMM_PAD_SCRATCH)
         sh_ctx = (a_s, h_s)
     if S and not fused:
         _lib.call("moe_combine", y.data_ptr(), _lib.MOE_BF16, S, M, E, k, cap, ids.data_ptr(),
@@ -171,7 +174,7 @@ def backward(layer, dout: torch.Tensor) -> dict:
         _gemm(dy, E * cap, M, w2o, F, None, dA, E, cap, load, 0, cap, _lib.MOE_ACT_GELU_BWD,
               c["a"])
         dxr = torch.empty((E * cap, M), dtype=torch.bfloat16, device=dev)
-        _gemm(dA, E * cap, F, w1o, M, None, dxr, E, cap, load, 0, cap)
+        _gemm(dA, E * cap, F, w1o, M, None, dxr, E, cap, load, 0, cap, _lib.MOE_GEMM_PAD_SCRATCH)
         # weight gradients: contract over each expert's kept rows, read MN-major
         # straight from the saved activations
         db2 = _colsum(dy, M, E, cap, load, 0)
@@ -193,7 +196,7 @@ def backward(layer, dout: torch.Tensor) -> dict:
     if S:
         _lib.call("moe_gate_bwd", c["logits"].data_ptr(), S, E, epad, k, ids.data_ptr(),
                   slots.data_ptr(), dp.data_ptr(), dlog.data_ptr(), 1, st)
-        _gemm(dlog, S, 2 * epad, wgo, M, None, dxg, 1, 0, None, S, S)
+        _gemm(dlog, S, 2 * epad, wgo, M, None, dxg, 1, 0, None, S, S, _lib.MOE_GEMM_PAD_SCRATCH)
         _lib.call("moe_gemm_bf16_wgrad_f32", x.data_ptr(), S, M, dlog.data_ptr(), 2 * epad,
                   dwg.data_ptr(), st)
     grads["gate_w"] = dwg[:, :E] + dwg[:, epad:epad + E]  # hi + lo (fp32)
@@ -205,7 +208,7 @@ def backward(layer, dout: torch.Tensor) -> dict:
         dA_s = torch.empty((S, F), dtype=torch.bfloat16, device=dev)
         _gemm(dout, S, M, s2o, F, None, dA_s, 1, 0, None, S, S, _lib.MOE_ACT_GELU_BWD, a_s)
         dxs = torch.empty((S, M), dtype=torch.bfloat16, device=dev)
-        _gemm(dA_s, S, F, s1o, M, None, dxs, 1, 0, None, S, S)
+        _gemm(dA_s, S, F, s1o, M, None, dxs, 1, 0, None, S, S, _lib.MOE_GEMM_PAD_SCRATCH)
         sdb2 = _colsum(dout, M, 1, 0, None, S)
         sdb1 = _colsum(dA_s, F, 1, 0, None, S)
         sdw2 = _wgrad(h_s, F, dout, M, 1, 0, None, S)[0]
