@@ -756,8 +756,12 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         if constexpr (kLoadX) load_x(0, xbuf[0]);
         // TMEM loads double-buffered across 32-column chunks: the load of
         // chunk c+1 is in flight while chunk c is biased, activated and stored.
-        uint32_t r[2][32];
-        tmem_ld_32x32b_x32(t_lane + tmem_col(0), r[0]);
+        // kSplit: a whole part is read into registers (kCP x 32 columns) and its
+        // TMEM handed straight back, so the MMAs refill it while the epilogue
+        // computes (the GELU drain is MUFU-bound and outlasts the MMA run-ahead)
+        constexpr int kRB = kSplit ? kCP : 2;
+        uint32_t r[kRB][32];
+        if constexpr (!kSplit) tmem_ld_32x32b_x32(t_lane + tmem_col(0), r[0]);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
           const int cl = chunk_col(c);  // column inside the tile
@@ -765,18 +769,24 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           if constexpr (kLoadX) {
             if (c + 1 < kChunks) load_x(c + 1, xbuf[(c + 1) & 1]);
           }
-          tmem_ld_wait_regs(r[c & 1]);
           if constexpr (kSplit) {
-            if (c % kCP == kCP - 1 && c + 1 < kChunks) {
-              // part c/kCP read out: hand it back to the MMA, then wait for the next part
+            if (c % kCP == 0) {
+              if (c > 0) {
+                mbar_wait(&tfull[c / kCP], acc_phase);
+                tc_fence_after();
+              }
+#pragma unroll
+              for (int e = 0; e < kCP; ++e) tmem_ld_32x32b_x32(t_lane + tmem_col(c + e), r[e]);
+#pragma unroll
+              for (int e = 0; e < kCP; ++e) tmem_ld_wait_regs(r[e]);
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive_cluster(&tempty[c / kCP], pl);
-              mbar_wait(&tfull[c / kCP + 1], acc_phase);
-              tc_fence_after();
             }
+          } else {
+            tmem_ld_wait_regs(r[c & 1]);
+            if (c + 1 < kChunks) tmem_ld_32x32b_x32(t_lane + tmem_col(c + 1), r[(c + 1) & 1]);
           }
-          if (c + 1 < kChunks) tmem_ld_32x32b_x32(t_lane + tmem_col(c + 1), r[(c + 1) & 1]);
           // whole warp: 32 rows x 32 columns -> smem (row = lane, 64 B, 64-B swizzle)
           // -> one TMA tensor store; rows / columns past the group's block are
           // clipped by the 3-D map (N, rows per group, G)
@@ -805,8 +815,8 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i)
                 pk32[i] = kzero ? 0u
-                                : pack_bf16x2(__uint_as_float(r[c & 1][2 * i]),
-                                              __uint_as_float(r[c & 1][2 * i + 1]));
+                                : pack_bf16x2(__uint_as_float(r[c % kRB][2 * i]),
+                                              __uint_as_float(r[c % kRB][2 * i + 1]));
               stage_store(pk32);
             }
             continue;
@@ -820,10 +830,10 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           for (int q = 0; q < 8; ++q) {
             const float4 bq = b4[q];
             constexpr float sc = EPI == EPI_BIAS_GELU ? 0.5f : 1.f;
-            v[4 * q + 0] = fmaf(__uint_as_float(r[c & 1][4 * q + 0]), sc, bq.x);
-            v[4 * q + 1] = fmaf(__uint_as_float(r[c & 1][4 * q + 1]), sc, bq.y);
-            v[4 * q + 2] = fmaf(__uint_as_float(r[c & 1][4 * q + 2]), sc, bq.z);
-            v[4 * q + 3] = fmaf(__uint_as_float(r[c & 1][4 * q + 3]), sc, bq.w);
+            v[4 * q + 0] = fmaf(__uint_as_float(r[c % kRB][4 * q + 0]), sc, bq.x);
+            v[4 * q + 1] = fmaf(__uint_as_float(r[c % kRB][4 * q + 1]), sc, bq.y);
+            v[4 * q + 2] = fmaf(__uint_as_float(r[c % kRB][4 * q + 2]), sc, bq.z);
+            v[4 * q + 3] = fmaf(__uint_as_float(r[c % kRB][4 * q + 3]), sc, bq.w);
           }
           if constexpr (EPI == EPI_WGRAD_ACC) {  // split-K partial: fp32 reduction in HBM/L2
             if (kzero) continue;
@@ -876,12 +886,12 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               const __nv_bfloat16* ab = reinterpret_cast<const __nv_bfloat16*>(xbuf[c & 1]);
 #pragma unroll
               for (int i = 0; i < 32; ++i)
-                v[i] = __uint_as_float(r[c & 1][i]) * gelu_tanh_grad_fast(__bfloat162float(ab[i]));
+                v[i] = __uint_as_float(r[c % kRB][i]) * gelu_tanh_grad_fast(__bfloat162float(ab[i]));
             } else {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
                 if (col0 + i < N)
-                  v[i] = __uint_as_float(r[c & 1][i]) *
+                  v[i] = __uint_as_float(r[c % kRB][i]) *
                          gelu_tanh_grad_fast(__bfloat162float(xrow[col0 + i]));
             }
           }
@@ -944,14 +954,16 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               if (col0 + i < N) drow[col0 + i] = __float2bfloat16_rn(v[i]);
           }
         }
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (CG == 2)
-            mbar_arrive_cluster(&tempty[kSplit ? kParts - 1 : acc], pl);  // the leader's MMA reuses it
-          else
-            mbar_arrive(&tempty[acc]);
+        if constexpr (!kSplit) {  // (kSplit handed every part back as it was read)
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2)
+              mbar_arrive_cluster(&tempty[acc], pl);  // the leader's MMA reuses it
+            else
+              mbar_arrive(&tempty[acc]);
+          }
         }
       } else {
         // ---------------- gate epilogue: thread = token row, BN >= E columns
@@ -1485,14 +1497,19 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
 #define MOE_FWD_EW 8
 #endif
     // MOE_BN512: 256 x 512 pair tiles (25% less operand traffic per flop) for
-    // 0 none, 1 every eligible forward GEMM, 2 (default) the plain-bias ones: the
-    // GELU epilogue's tanh (MUFU-bound) drains a half slower than the MMAs refill
-    // it, the bias-only epilogue keeps up (C2 / C4 +3-5%, GEMM1 at C3 -2%)
+    // 0 none, 1 every eligible forward GEMM incl. the fused combine, 2 the
+    // plain-bias ones, 3 (default) plain-bias + bias/GELU launches of >= 1 TFLOP.
+    // Measured: plain-bias C2 / C4 +3-5%; GEMM1 (GELU, its epilogue staging each
+    // accumulator half in registers) wins only where the launch is long enough to
+    // run at the 1 kW cap, where operand traffic is energy (C3: layer +1%, GEMM1
+    // up to -4%), and loses 5-10% at full clock (C2 / C4 GEMM1); the fused combine
+    // is 2% slower on it (mode 1 only)
     static const int bn512 = [] {
       const char* v = getenv("MOE_BN512");
-      return v ? atoi(v) : 2;
+      return v ? atoi(v) : 3;
     }();
-    if ((bn512 == 1 || (bn512 == 2 && !gelu)) && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
+    const bool long_launch = 2.0 * (double)G * (double)max_group_rows * N * K >= 1e12;
+    if ((bn512 == 1 || (bn512 >= 2 && !gelu) || (bn512 == 3 && long_launch)) && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
         (N % 512) == 0 && make_map_out3d(&md, D, G, per_group, N) == 0) {
       // 256 x 512 pair tiles; TMEM holds one accumulator, handed over in two halves
       CUtensorMap mb2;
