@@ -193,3 +193,23 @@ def test_grouped_gemm_bf16_gather(K, N, act, cap):
     for g, r in enumerate(rows):
         got, want = d[g * cap:g * cap + r], d2[g * cap:g * cap + r]
         assert torch.equal(got, want), (g, (got.float() - want.float()).abs().max().item())
+
+
+@pytest.mark.parametrize("bn512", ["0", "1"])
+def test_tile_variants_env(bn512):
+    """The expert-GEMM tile choice is read from MOE_BN512 once per process: rerun
+    the grouped-GEMM and fused-combine layer parity tests in a child process with
+    every 256x512 path forced on (1: bias, bias+GELU at any size, fused combine)
+    and with all of them off (0)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MOE_BN512=bn512, PYTHONDONTWRITEBYTECODE="1")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+           "tests/test_gpu_gemm.py::test_grouped_gemm_bf16",
+           "tests/test_gpu_layer.py::test_fused_combine_matches_unfused",
+           "tests/test_gpu_layer.py::test_bf16_layers_sampled"]
+    res = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
