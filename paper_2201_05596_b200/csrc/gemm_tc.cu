@@ -1092,7 +1092,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           args.local_rank[t * k] = r0;
           if (k == 2) args.local_rank[t * k + 1] = r1;
         }
-        const int64_t tile_row0 = (int64_t)mb * TM + cta * BM;  // this CTA's routing tile
+        const int64_t tile_row0 = (int64_t)mb * TMC + pair * TM + cta * BM;  // this CTA's routing tile
         if (tile_row0 < args.S)
           for (int e = tid; e < E; e += 128)
             args.tile_counts[tile_row0 / kRouteTile * E + e] =
@@ -1645,10 +1645,17 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   // stage) so the smem ring holds more x bytes in flight per SM (the gate is
   // HBM-latency bound: 66 -> ~52 us at C3 measured for the smaller-B configs)
   const int CG = BN >= 128 ? 2 : 1;
+  // MOE_GATE_CL4=1 (E > 64): 4-CTA clusters, two pairs on consecutive 256-token
+  // blocks sharing W_g^T by TMA multicast (each CTA loads a quarter per stage)
+  static const int cl4_env = [] {
+    const char* v = getenv("MOE_GATE_CL4");
+    return v ? atoi(v) : 0;
+  }();
+  const int CLP = (cl4_env == 1 && CG == 2) ? 2 : 1;
   CUtensorMap ma, mb;
   int rc = make_map(&ma, x, S, M, BM);
   if (rc) return rc;
-  rc = make_map(&mb, wg_t, BN, M, BN / CG);  // wg_t is padded to BN rows
+  rc = make_map(&mb, wg_t, BN, M, BN / CG / CLP);  // wg_t is padded to BN rows
   if (rc) return rc;
   GemmArgs a{};
   a.K = M;
@@ -1666,7 +1673,10 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   a.tile_counts = tile_counts;
   a.probsum = probsum;
   a.prefetch = prefetch_mode() & 1 ? 1 : 0;
-  const int64_t tiles = (S + (int64_t)BM * CG - 1) / ((int64_t)BM * CG);
+  const int64_t tiles = (S + (int64_t)BM * CG * CLP - 1) / ((int64_t)BM * CG * CLP);
+  if (CLP == 2)
+    return BN == 128 ? launch_tc<128, 8, EPI_GATE, 2, 4, 4>(ma, mb, a, tiles, st)
+                     : launch_tc<256, 6, EPI_GATE, 2, 4, 4>(ma, mb, a, tiles, st);
   switch (BN) {
     case 32: return launch_tc<32, 8, EPI_GATE>(ma, mb, a, tiles, st);
     case 64: return launch_tc<64, 8, EPI_GATE>(ma, mb, a, tiles, st);
