@@ -651,6 +651,18 @@ static void combine_vec(bool expert_order, int g, int threads, cudaStream_t st, 
     const char* v = getenv("MOE_COMBINE_TPW");
     return v ? atoi(v) : 2;
   }();
+  if (tpw == 4 && VEC > 1) {
+    const int g4 = (g + 3) / 4;
+    if (expert_order)
+      combine_kernel<T, P, true, VEC, 4><<<g4, threads, 0, st>>>(
+          (const T*)y, S, M, k, E, cap, ids, slots, row_index, (const P*)gp, (const T*)x,
+          (const T*)shared, (T*)out);
+    else
+      combine_kernel<T, P, false, VEC, 4><<<g4, threads, 0, st>>>(
+          (const T*)y, S, M, k, E, cap, ids, slots, row_index, (const P*)gp, (const T*)x,
+          (const T*)shared, (T*)out);
+    return;
+  }
   if (tpw == 2 && VEC > 1) {
     const int g2 = (g + 1) / 2;
     if (expert_order)
