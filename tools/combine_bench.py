@@ -29,10 +29,10 @@ for name, S, M, E, k, cap, res in [("c2", 16384, 1024, 16, 2, 2560, False),
     for _ in range(5):
         run()
     torch.cuda.synchronize()
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush = torch.ones(64 << 20, dtype=torch.int64, device="cuda")  # 512 MB
     ts = []
     for _ in range(30):  # L2 flushed before every launch, median
-        flush.zero_()
+        flush.max()  # read-only flush: evicts without leaving dirty lines to write back
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         run()

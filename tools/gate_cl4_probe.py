@@ -24,7 +24,7 @@ mode = os.environ.get("MOE_GATE_CL4", "0")
 S, M = 65536, 2048
 torch.manual_seed(0)
 x = torch.randn(S, M, device="cuda").to(torch.bfloat16)
-flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+flush = torch.ones(64 << 20, dtype=torch.int64, device="cuda")  # 512 MB
 saved = {}
 for E in (128, 256):
     wg = (torch.randn(E, M, device="cuda") * 0.02).to(torch.bfloat16)
@@ -49,7 +49,7 @@ for E in (128, 256):
                   ids.data_ptr(), gp.data_ptr(), lr.data_ptr(), tc.data_ptr(), _lib.stream_ptr())
         ts = []
         for _ in range(40):
-            flush.zero_()
+            flush.max()  # read-only flush: evicts without leaving dirty lines to write back
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             _lib.call("moe_gate_gemm_bf16", x.data_ptr(), wg.data_ptr(), S, M, E, k, None,
