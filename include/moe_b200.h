@@ -11,10 +11,18 @@
  *
  * Conventions
  *  - All pointers are DEVICE pointers on the current CUDA device, allocated
- *    by the caller (the library never allocates or frees). `stream` is a
+ *    by the caller (the library does not allocate caller data). `stream` is a
  *    cudaStream_t passed as void*; every call is stream-ordered and
- *    asynchronous. The library holds no global mutable state besides cached
- *    driver entry points, so calls are reentrant ("pure").
+ *    asynchronous. Results depend only on the arguments (SPEC.md:198-199
+ *    "pure"). The library does keep process-wide launch caches, all keyed by
+ *    device ordinal and thread-safe: per-(kernel, device) dynamic-smem
+ *    attributes, SM counts and resident-cluster counts, a per-device pool of
+ *    device-side tile counters (dynamic GEMM scheduling) and a per-device side
+ *    stream; plus the cuTensorMapEncodeTiled entry point and the MOE_* tuning
+ *    environment variables, read once. One process may drive several GPUs
+ *    from several threads.
+ *  - Exception: moe_malloc-style helpers (moe_ipc_malloc/free, for peer-memory
+ *    regions) allocate, because a cudaIpc handle needs its own allocation.
  *  - Routing tables are int32 on device: ids/slots/local_rank are (S, k)
  *    row-major, token-major flattening (gating.py:226). DROPPED slot = -1.
  *  - Return value: 0 on success, MOE_EINVAL for bad arguments (checked before

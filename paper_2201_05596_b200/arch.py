@@ -498,8 +498,14 @@ def load_balance_loss(plan, probs) -> float:
     pd = _dev(p)
     if pd.dtype not in (torch.float32, torch.float64):
         pd = pd.float()
-    ids = _dev(np.asarray(plan.expert_ids, dtype=np.int32) if not _is_torch(plan.expert_ids)
-               else plan.expert_ids, torch.int32).to(pd.device)
+    raw = plan.expert_ids
+    if (bool(((raw < 0) | (raw >= e)).any()) if _is_torch(raw) else
+            bool(np.any((np.asarray(raw) < 0) | (np.asarray(raw) >= e)))):
+        # np.bincount rejects negative ids and longer counts do not broadcast
+        # against the E mean probabilities (arch.py:310-313)
+        raise ValueError(f"expert ids must lie in [0, {e})")
+    ids = _dev(np.asarray(raw, dtype=np.int32) if not _is_torch(raw) else raw,
+               torch.int32).to(pd.device)
     lib = _lib.load()
     wsb = lib.moe_load_balance_workspace_bytes(e)
     ws = torch.empty(wsb // 8, dtype=torch.float64, device=pd.device)

@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
 
 namespace moe {
@@ -996,6 +997,33 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               if (c * 32 + i < E) lrow[c * 32 + i] = __uint_as_float(r[i]);
           }
         }
+        // Rows with fewer than k values above -inf (NaN / -inf logits, e.g. after a
+        // diverged step) re-rank with np.argsort(-logits, kind="stable") semantics:
+        // NaN after every number, -inf before NaN, ties to the lower index - so
+        // every id stays inside [0, E). Warp-uniform (tcgen05.ld is collective).
+        const bool slow = i1 == 0x7fffffff || (args.k == 2 && i2 == 0x7fffffff);
+        if (__any_sync(0xffffffffu, slow)) {
+          float s1 = 0.f, s2 = 0.f;
+          int j1 = -1, j2 = -1;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(t_addr + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll 1
+            for (int i = 0; i < 32; ++i) {
+              const int col = c * 32 + i;
+              if (col >= E) break;
+              const float v = __uint_as_float(r[i]);
+              const bool vn = v != v;
+              const bool g1 = j1 < 0 || (!vn && ((s1 != s1) || v > s1));
+              const bool g2 = !g1 && (j2 < 0 || (!vn && ((s2 != s2) || v > s2)));
+              if (g1) { s2 = s1; j2 = j1; s1 = v; j1 = col; }
+              else if (g2) { s2 = v; j2 = col; }
+            }
+          }
+          if (slow) { b1 = s1; i1 = j1; b2 = s2; i2 = j2; }
+        }
         float sum = 0.f;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
@@ -1297,14 +1325,41 @@ static bool side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join) {
   return true;
 }
 
+// Per-device launch facts, cached per device ordinal (the library targets the
+// current device; one process may drive several GPUs, from several threads).
+constexpr int kMaxDevices = 64;
+
+static int cur_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return -1;
+  return dev;
+}
+
 static int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<int> n[kMaxDevices];
+  const int dev = cur_device();
+  if (dev < 0) return 148;
+  int v = n[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1)
+      v = 148;
+    n[dev].store(v, std::memory_order_relaxed);
   }
-  return n;
+  return v;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) binds to the current device's
+// context: set it once per (kernel instance, device). Setting it twice is benign,
+// so concurrent first calls only race to do the same work.
+template <typename Kern>
+static cudaError_t ensure_smem_attr(Kern kern, int bytes, std::atomic<uint64_t>& done_mask) {
+  const int dev = cur_device();
+  if (dev < 0) return cudaErrorInvalidDevice;
+  const uint64_t bit = 1ull << dev;
+  if (done_mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_release);
+  return e;
 }
 
 template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4, int CL = CG, int SUB = 1>
@@ -1313,11 +1368,10 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
                      int64_t grid_cap = 0) {
   using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>()>;
   auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW, CL, SUB>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+  static std::atomic<uint64_t> attr_done{0};
+  {
+    cudaError_t e = ensure_smem_attr(kern, L::kTotal, attr_done);
     if (e != cudaSuccess) return (int)e;
-    attr_done = true;
   }
   int64_t grid = num_sms();
   if (gemm_cta_limit() > 0 && gemm_cta_limit() < grid) grid = gemm_cta_limit();
@@ -1339,11 +1393,14 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   cfg.numAttrs = 1;
   if constexpr (CL > 2) {
     // 4-CTA clusters must fit whole GPCs: size the persistent grid to what can be resident
-    static int max_clusters = 0;
+    static std::atomic<int> clusters_by_dev[kMaxDevices];
+    const int dev = cur_device();
+    int max_clusters = dev >= 0 ? clusters_by_dev[dev].load(std::memory_order_relaxed) : 0;
     if (max_clusters == 0) {
       if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess ||
           max_clusters < 1)
         max_clusters = (int)(num_sms() / CL);
+      if (dev >= 0) clusters_by_dev[dev].store(max_clusters, std::memory_order_relaxed);
     }
     if (grid > (int64_t)max_clusters * CL) grid = (int64_t)max_clusters * CL;
     cfg.gridDim = dim3((unsigned)grid);
@@ -1354,8 +1411,10 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
 
 // Resident 4-CTA clusters of the forward GEMM (B200: 33 -> 132 of 148 SMs).
 static int max_clusters4(bool gelu) {
-  static int n[2] = {0, 0};
-  int& v = n[gelu ? 1 : 0];
+  static std::atomic<int> n[kMaxDevices][2];
+  const int dev = cur_device();
+  if (dev < 0) return num_sms() / 4;
+  int v = n[dev][gelu ? 1 : 0].load(std::memory_order_relaxed);
   if (v == 0) {
     using L = Smem<256, 5, 2, out_stage_bytes<EPI_BIAS, 8, 2, 256>()>;
     cudaLaunchConfig_t cfg{};
@@ -1371,9 +1430,11 @@ static int max_clusters4(bool gelu) {
     cfg.numAttrs = 1;
     auto kern = gelu ? gemm_bf16_tc_kernel<256, 5, EPI_BIAS_GELU, 2, 8, 4>
                      : gemm_bf16_tc_kernel<256, 5, EPI_BIAS, 2, 8, 4>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    static std::atomic<uint64_t> attr_done[2];
+    ensure_smem_attr(kern, L::kTotal, attr_done[gelu ? 1 : 0]);
     if (cudaOccupancyMaxActiveClusters(&v, kern, &cfg) != cudaSuccess || v < 1)
       v = num_sms() / 4;
+    n[dev][gelu ? 1 : 0].store(v, std::memory_order_relaxed);
   }
   return v;
 }
@@ -1460,6 +1521,10 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
     }
   }
   if (act == 2) {  // fused combine epilogue
+#ifdef MOE_EXPERIMENTAL_BN512_COMBINE
+    // 256 x 512 fused-combine tiles: measured 2% slower than 256 x 256 and they
+    // spill (684 B stores / 1152 B loads), so they are only compiled on request
+    // (MOE_BUILD_EXPERIMENTAL=1 at build time) and then selected by MOE_BN512=1
     static const int bn512c = [] {
       const char* v = getenv("MOE_BN512");
       return v ? atoi(v) : 0;
@@ -1471,6 +1536,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
       const int64_t tiles512 = (int64_t)G * ((max_group_rows + tm - 1) / tm) * ((N + 511) / 512);
       return launch_tc<512, 4, EPI_BIAS_COMBINE, 2, 8>(ma, mb2, a, tiles512, st);
     }
+#endif
     if (CG == 2) return launch_tc<256, 6, EPI_BIAS_COMBINE, 2, 8>(ma, mb, a, max_tiles, st);
     switch (BN) {
       case 32: return launch_tc<32, 8, EPI_BIAS_COMBINE, 1, 4>(ma, mb, a, max_tiles, st);

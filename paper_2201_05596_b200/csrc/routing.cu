@@ -17,10 +17,24 @@ namespace moe {
 
 // ============================================================ top-k gate
 // One warp per token row. Lane l owns columns l, l+32, ... (coalesced).
+constexpr int kNoExpert = 0x7fffffff;
+
+// Order of np.argsort(-logits, kind="stable") (gating.py:159-161): descending
+// value, ties to the lower expert index, NaN after every number (numpy sorts
+// NaN last) - so a row of NaN / -inf still routes to valid expert indices.
+template <typename T>
+MOE_DEV bool ranks_before(T v, int i, T bv, int bi) {
+  if (i == kNoExpert) return false;
+  if (bi == kNoExpert) return true;
+  const bool vn = v != v, bn = bv != bv;
+  if (vn != bn) return bn;
+  if (!vn && v != bv) return v > bv;
+  return i < bi;
+}
+
 template <typename T>
 MOE_DEV void better(T v, int i, T& bv, int& bi) {
-  // descending value, ties to the lower expert index (gating.py:159-161)
-  if (v > bv || (v == bv && i < bi)) {
+  if (ranks_before(v, i, bv, bi)) {
     bv = v;
     bi = i;
   }
@@ -50,11 +64,11 @@ __global__ void topk_gate_kernel(const T* __restrict__ logits, int64_t S, int E,
     const T* row = logits + t * E;
     const T ninf = -INFINITY;
     T b1 = ninf;
-    int i1 = 0x7fffffff;
+    int i1 = kNoExpert;
     for (int c = lane; c < E; c += 32) better(row[c], c, b1, i1);
     warp_argmax(b1, i1);
     T b2 = ninf;
-    int i2 = 0x7fffffff;
+    int i2 = kNoExpert;
     if (k == 2) {
       for (int c = lane; c < E; c += 32)
         if (c != i1) better(row[c], c, b2, i2);
@@ -98,8 +112,14 @@ __global__ void plan_tiles_kernel(const int32_t* __restrict__ ids, int64_t S, in
   for (int i = tid; i < 4 * E; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
   const bool valid = t < S;
+  // an id outside [0, E) matches no expert's indicator in the reference
+  // (gating.py:229-230): it takes no slot and stays DROPPED
   int e0 = valid ? ids[t * k] : -1;
   int e1 = (valid && k == 2) ? ids[t * k + 1] : -2;
+  const bool v0 = valid && e0 >= 0 && e0 < E;
+  const bool v1 = valid && k == 2 && e1 >= 0 && e1 < E;
+  if (!v0) e0 = -1;
+  if (!v1) e1 = -2;
   int r0 = 0, r1 = 0;
   if (k == 1) {
     r0 = warp_rank_same(e0, lane);
@@ -112,17 +132,16 @@ __global__ void plan_tiles_kernel(const int32_t* __restrict__ ids, int64_t S, in
         r1 += (o0 == e1) + (o1 == e1);
       }
     }
+    r1 += (e0 == e1);  // a hand-built gate may repeat an expert: choice 0 comes first
   }
-  if (valid) {
-    atomicAdd(&cnt[w * E + e0], 1);
-    if (k == 2) atomicAdd(&cnt[w * E + e1], 1);
-  }
+  if (v0) atomicAdd(&cnt[w * E + e0], 1);
+  if (v1) atomicAdd(&cnt[w * E + e1], 1);
   __syncthreads();
   if (valid) {
-    for (int q = 0; q < w; ++q) {
-      r0 += cnt[q * E + e0];
-      if (k == 2) r1 += cnt[q * E + e1];
-    }
+    if (v0)
+      for (int q = 0; q < w; ++q) r0 += cnt[q * E + e0];
+    if (v1)
+      for (int q = 0; q < w; ++q) r1 += cnt[q * E + e1];
     local_rank[t * k] = r0;
     if (k == 2) local_rank[t * k + 1] = r1;
   }
@@ -184,6 +203,10 @@ __global__ void plan_slots_kernel(const int32_t* __restrict__ ids,
        a += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = a / k;
     const int e = ids[a];
+    if (e < 0 || e >= E) {  // matches no expert (plan_tiles_kernel)
+      slots[a] = -1;
+      continue;
+    }
     const int64_t slot = (int64_t)tile_offsets[(t / kRouteTile) * E + e] + local_rank[a];
     slots[a] = slot < cap ? (int32_t)slot : -1;
   }
@@ -483,8 +506,10 @@ __global__ void aux_stats_kernel(const int32_t* __restrict__ ids, int64_t S, int
     for (int64_t r = r0; r < r1; ++r) acc += (double)probs[r * E + c];
     if (r1 > r0) atomicAdd(&ws[c], acc);
   }
-  for (int64_t a = r0 * k + threadIdx.x; a < r1 * k; a += blockDim.x)
-    atomicAdd(&ws[E + ids[a]], 1.0);
+  for (int64_t a = r0 * k + threadIdx.x; a < r1 * k; a += blockDim.x) {
+    const int e = ids[a];
+    if (e >= 0 && e < E) atomicAdd(&ws[E + e], 1.0);  // the host rejects others first
+  }
 }
 
 __global__ void aux_finalize_kernel(int64_t S, int k, int E, const double* __restrict__ ws,

@@ -52,7 +52,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .arch import FFN_MULT, DenseFfn, LayerSpec, MoeLayerParams, _Phases, _t
-from .exchange import Exchanger, ReplicaMismatchError
+from .exchange import Exchanger, ReplicaMismatchError, _a2a, all_gather_flat, all_reduce_sum
 from .gating import GatingConfig
 from .tensor import ShapeError
 
@@ -123,16 +123,13 @@ def rank_counts(plan: ExchangePlan) -> np.ndarray:
 
 def gather_counts(out_flat: torch.Tensor, totals: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather every rank's (E,) expert counts into a flat (world*E,) tensor."""
-    dist.all_gather_into_tensor(out_flat, totals, group=group)
+    all_gather_flat(out_flat, totals, group=group)
     return out_flat.view(-1, totals.numel())
 
 
 def exchange_rows(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group=None):
     """One flat all-to-all of variable row counts (NCCL on GPU, gloo on CPU)."""
-    n_out, n_in = int(sum(out_splits)), int(sum(in_splits))
-    dist.all_to_all_single(out[:n_out], inp[:n_in], output_split_sizes=list(out_splits),
-                           input_split_sizes=list(in_splits), group=group)
-    return out[:n_out]
+    return _a2a(out, inp, out_splits, in_splits, group)
 
 
 class EPMoeLayer:
@@ -377,6 +374,7 @@ class EPMoeLayer:
 
     def kept_assignments(self, S: int) -> int:
         if self.transport == "p2p":
+            self.check_errors()  # syncs anyway: surface a timed-out peer barrier here
             if self.chunks > 1:
                 return int(self._p2p[S]["kept_c"].sum().item())
             return int(self._ws[S]["kept"].sum().item())
@@ -393,7 +391,7 @@ class EPMoeLayer:
         # the peer-memory layout is sized from the global batch: all ranks equal S
         sizes = torch.tensor([S], dtype=torch.int64, device=self.dev)
         alls = torch.empty(self.world, dtype=torch.int64, device=self.dev)
-        dist.all_gather_into_tensor(alls, sizes, group=self.group)
+        all_gather_flat(alls, sizes, group=self.group)
         if int(alls.min()) != int(alls.max()):
             raise ValueError("the peer-memory transport needs the same token count on every rank")
         from .ipc import IpcRegion
@@ -655,6 +653,7 @@ class EPMoeLayer:
         if self.transport == "p2p":
             from types import SimpleNamespace
 
+            self.check_errors()
             st = self._p2p[S]
             load = st["seg_rows"].cpu().numpy()
             load = load.reshape(self.chunks, self.E_loc).sum(axis=0)
@@ -821,7 +820,7 @@ class SlicedEPMoeLayer(EPMoeLayer):
                       max_rows, _lib.MOE_ACT_NONE, st)
             if L > 1:
                 ph("slice_allreduce")
-                dist.all_reduce(y, group=self.exchanger.slice_group)
+                all_reduce_sum(y, group=self.exchanger.slice_group)
         ph("coordinated_return")
         self.exchanger.coordinated(ws["ret"], ws["y"], Cg.T)
         ph("combine")

@@ -38,7 +38,8 @@ import torch.distributed as dist
 from . import _lib
 
 __all__ = ["ScheduleError", "ReplicaMismatchError", "ExchangeStats", "Exchanger",
-           "hierarchical_plan", "coordinated_plan"]
+           "hierarchical_plan", "coordinated_plan", "device_collectives", "all_gather_flat",
+           "all_reduce_sum"]
 
 
 class ScheduleError(ValueError):
@@ -101,10 +102,50 @@ def _gather(dst: torch.Tensor, src: torch.Tensor, idx: np.ndarray) -> torch.Tens
     return dst[:n]
 
 
+def device_collectives(group=None) -> bool:
+    """NCCL groups move device tensors directly. Gloo groups move host tensors:
+    the CPU tests, and several ranks sharing ONE GPU (NCCL refuses duplicate
+    devices; the single-GPU EP parity test runs that way) - device tensors
+    are staged through host memory there."""
+    return dist.get_backend(group) == "nccl"
+
+
+def _staged(t: torch.Tensor, group) -> bool:
+    return t.is_cuda and not device_collectives(group)
+
+
+def all_gather_flat(out: torch.Tensor, inp: torch.Tensor, group=None) -> torch.Tensor:
+    """out[r*n:(r+1)*n] = inp of rank r (out is (world*n, ...) contiguous)."""
+    if _staged(inp, group):
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+    return out
+
+
+def all_reduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
+    if _staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
+    return t
+
+
 def _a2a(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group) -> torch.Tensor:
     n_out, n_in = int(sum(out_splits)), int(sum(in_splits))
-    dist.all_to_all_single(out[:n_out], inp[:n_in], output_split_sizes=[int(v) for v in out_splits],
-                           input_split_sizes=[int(v) for v in in_splits], group=group)
+    osz, isz = [int(v) for v in out_splits], [int(v) for v in in_splits]
+    if _staged(inp, group):
+        o = torch.empty((n_out,) + tuple(out.shape[1:]), dtype=out.dtype)
+        dist.all_to_all_single(o, inp[:n_in].cpu(), output_split_sizes=osz, input_split_sizes=isz,
+                               group=group)
+        out[:n_out].copy_(o)
+    else:
+        dist.all_to_all_single(out[:n_out], inp[:n_in], output_split_sizes=osz,
+                               input_split_sizes=isz, group=group)
     return out[:n_out]
 
 
@@ -272,11 +313,7 @@ class Exchanger:
         _a2a(pad, send1, pl["out1"], pl["in1"], self.rail_group)
         gbuf = self._buf("gath", L * maxh, inp)[:L * maxh]
         if L > 1:
-            if dist.get_backend(self.slice_group) == "nccl":
-                dist.all_gather_into_tensor(gbuf, pad[:maxh], group=self.slice_group)
-            else:
-                dist.all_gather(list(gbuf.view(L, maxh, *inp.shape[1:]).unbind(0)), pad[:maxh],
-                                group=self.slice_group)
+            all_gather_flat(gbuf, pad[:maxh], group=self.slice_group)
         else:
             gbuf = pad[:maxh]
         # reassemble each source block: position i came from member i % L

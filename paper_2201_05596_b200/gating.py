@@ -202,6 +202,17 @@ def exclusive_scan_blelloch(values):
     return _host(tree[:n], np.float64) if as_np else tree[:n]
 
 
+def _route_ids(expert_ids, num_experts: int):
+    """int32 ids for the device; an id outside [0, E) matches no expert's
+    indicator in the reference (gating.py:229-230) and stays DROPPED, so it is
+    mapped to -1 here (before the int32 narrowing could alias it)."""
+    if _is_torch(expert_ids):
+        ids = expert_ids.to(torch.int64)
+        return torch.where((ids >= 0) & (ids < num_experts), ids, -1).to(torch.int32)
+    ids = np.asarray(expert_ids, dtype=np.int64)
+    return np.where((ids >= 0) & (ids < num_experts), ids, -1).astype(np.int32)
+
+
 def build_dispatch_plan(gates: TopKGate, cfg: GatingConfig, num_tokens: int) -> DispatchPlan:
     """Capacity slots in flattened token-major order, DROPPED past capacity
     (gating.py:211-247). Bit-exact with the reference for any ids."""
@@ -211,8 +222,7 @@ def build_dispatch_plan(gates: TopKGate, cfg: GatingConfig, num_tokens: int) -> 
             f"({num_tokens}, {cfg.k})")
     as_np = not _is_torch(gates.expert_ids)
     cap = cfg.capacity(num_tokens)
-    ids = _dev(np.asarray(gates.expert_ids, dtype=np.int32) if as_np else gates.expert_ids,
-               torch.int32)
+    ids = _dev(_route_ids(gates.expert_ids, cfg.num_experts), torch.int32)
     dev = ids.device
     slots = torch.empty((num_tokens, cfg.k), dtype=torch.int32, device=dev)
     load = torch.empty(cfg.num_experts, dtype=torch.int32, device=dev)
@@ -236,7 +246,15 @@ def _plan_tables(plan: DispatchPlan, dev) -> tuple[torch.Tensor, torch.Tensor]:
                else plan.expert_ids, torch.int32)
     slots = _dev(np.asarray(plan.slots, dtype=np.int32) if not _is_torch(plan.slots)
                  else plan.slots, torch.int32)
-    return ids.to(dev), slots.to(dev)
+    ids, slots = ids.to(dev), slots.to(dev)
+    # a kept assignment must address a real (expert, slot) row: the reference's
+    # fancy indexing raises on anything else (gating.py:271-275, :298-304)
+    kept = slots != DROPPED
+    bad = kept & ((ids < 0) | (ids >= plan.num_experts) | (slots < 0) |
+                  (slots >= plan.capacity))
+    if bool(bad.any()):
+        raise IndexError("plan has a kept assignment outside the (num_experts, capacity) buffers")
+    return ids, slots
 
 
 def scatter_tokens(batch, plan: DispatchPlan, counter: OpCounter | None = None) -> ExpertBuffers:

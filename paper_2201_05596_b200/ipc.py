@@ -1,7 +1,8 @@
 """Peer-memory regions shared by the ranks of a process group (one GPU each).
 
 Each rank cudaMallocs a region through libmoe_b200 (``moe_ipc_malloc``),
-all-gathers the 64-byte cudaIpc handles over the group (NCCL), and opens the
+all-gathers the 64-byte cudaIpc handles over the group (NCCL; gloo when several
+ranks share one GPU, which cudaIpc also supports), and opens the
 peers' handles, so every rank holds device pointers to every rank's region:
 NVLink loads/stores from kernels then go straight to the owner's HBM.
 """
@@ -53,9 +54,11 @@ class IpcRegion:
         self.local = p.value
         h = (ctypes.c_uint8 * 64)()
         _lib.check(lib.moe_ipc_get_handle(self.local, ctypes.addressof(h)), "moe_ipc_get_handle")
+        from .exchange import all_gather_flat
+
         mine = torch.tensor(np.frombuffer(bytes(h), dtype=np.uint8), device=self.device)
         allh = torch.empty(self.world * 64, dtype=torch.uint8, device=self.device)
-        dist.all_gather_into_tensor(allh, mine, group=group)
+        all_gather_flat(allh, mine, group=group)
         allh = allh.cpu().numpy().reshape(self.world, 64)
         self.ptrs = []
         for r in range(self.world):

@@ -106,6 +106,11 @@ class GraphedForward:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.y = layer(self.x, out=self.out)
+        # the captured kernels write into the layer's per-size workspaces: keep them
+        # alive even if the layer later evicts them for other batch sizes (a replay
+        # would otherwise write into memory the allocator has handed out again)
+        self._keep = [d.get(rows) for d in (getattr(layer, "_ws", None),
+                                            getattr(layer, "_p2p", None)) if d]
 
     def __call__(self, x: torch.Tensor) -> torch.Tensor:
         self.x.copy_(x, non_blocking=True)

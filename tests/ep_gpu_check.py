@@ -19,6 +19,8 @@ from paper_2201_05596_b200 import arch as A  # noqa: E402
 from paper_2201_05596_b200.ep import EPMoeLayer, SlicedEPMoeLayer  # noqa: E402
 from paper_2201_05596_b200.gating import GatingConfig  # noqa: E402
 
+SAME_DEVICE = os.environ.get("EP_SAME_DEVICE") == "1"
+
 
 def make_params(M, E, residual, skew, g, dev):
     F = 4 * M
@@ -69,7 +71,12 @@ def run_sliced(S_grp, M, E, k, cf, skew, seed, L):
     assert excess <= 0, f"sliced output off by {excess}"
     # every member of a group holds the same output
     peers = [torch.empty_like(got) for _ in range(world)]
-    dist.all_gather(peers, got)
+    if SAME_DEVICE:  # gloo: host tensors
+        hp = [torch.empty_like(got, device="cpu") for _ in range(world)]
+        dist.all_gather(hp, got.cpu())
+        peers = [h.to(got.device) for h in hp]
+    else:
+        dist.all_gather(peers, got)
     for u in range(L):
         assert torch.equal(peers[q * L + u], got), "group members disagree"
     st = layer.exchanger.last_stats
@@ -120,8 +127,16 @@ def run_case(S_loc, M, E, k, cf, residual, skew, seed, transport="auto", schedul
 
 
 def main():
-    dist.init_process_group("nccl")
-    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    if SAME_DEVICE:
+        # every rank on cuda:0 (the driver's 1-GPU test box): gloo bootstraps the
+        # ranks (NCCL refuses two ranks on one device), the p2p transport maps
+        # the other processes' regions with same-device cudaIpc, and its counts
+        # all-gather and barriers run over that peer memory exactly as on NVLink
+        dist.init_process_group("gloo")
+        torch.cuda.set_device(0)
+    else:
+        dist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     world = dist.get_world_size()
     cases = [
         (4096, 1024, 16, 2, 1.25, False, 0.5, 1),
@@ -136,7 +151,7 @@ def main():
                 continue
             dropped = run_case(*c, transport=transport)
             if dist.get_rank() == 0:
-                print(f"ep ok world={world} transport={transport} case={c} "
+                print(f"ep ok same_device={int(SAME_DEVICE)} world={world} transport={transport} case={c} "
                       f"dropped_on_rank0={dropped}", flush=True)
     # seeded random configurations, both transports where they apply
     rng = np.random.default_rng(2024 + world)
@@ -153,7 +168,7 @@ def main():
                 continue
             run_case(*c, transport=transport)
             if dist.get_rank() == 0:
-                print(f"ep ok world={world} random-case via {transport} case={c}", flush=True)
+                print(f"ep ok same_device={int(SAME_DEVICE)} world={world} random-case via {transport} case={c}", flush=True)
     # chunked p2p (dispatch / pull of neighbouring chunks beside the GEMMs): bit-identical
     for c in [(2048, 2048, 32, 1, 1.0, False, 0.0, 3), (2560, 1024, 16, 1, 0.8, False, 1.0, 5)]:
         for chunks in (2, 4):
@@ -161,14 +176,14 @@ def main():
                 continue
             dropped = run_case(*c, transport="p2p", chunks=chunks)
             if dist.get_rank() == 0:
-                print(f"ep ok world={world} transport=p2p-chunked chunks={chunks} case={c} "
+                print(f"ep ok same_device={int(SAME_DEVICE)} world={world} transport=p2p-chunked chunks={chunks} case={c} "
                       f"dropped_on_rank0={dropped}", flush=True)
     # hierarchical node/rail schedule (2 "nodes" of world/2 GPUs): bit-identical too
     if world % 2 == 0:
         for c in cases[:2] + cases[3:4]:
             run_case(*c, transport="nccl", schedule="hierarchical", gpus_per_node=world // 2)
             if dist.get_rank() == 0:
-                print(f"ep ok world={world} schedule=hierarchical G={world // 2} case={c}",
+                print(f"ep ok same_device={int(SAME_DEVICE)} world={world} schedule=hierarchical G={world // 2} case={c}",
                       flush=True)
     # tensor-sliced groups with expert slicing (coordinated exchange)
     sl_cases = [(2048, 1024, 8, 1, 1.0, 0.5, 11, 2), (1500, 512, 4, 2, 0.8, 1.0, 12, 2),
@@ -179,7 +194,7 @@ def main():
             continue
         st = run_sliced(*c)
         if dist.get_rank() == 0:
-            print(f"ep ok world={world} schedule=coordinated L={c[-1]} case={c} "
+            print(f"ep ok same_device={int(SAME_DEVICE)} world={world} schedule=coordinated L={c[-1]} case={c} "
                   f"rounds={st.a2a_rounds}+{st.allgather_rounds}", flush=True)
     dist.barrier()
     dist.destroy_process_group()

@@ -255,3 +255,101 @@ def test_fused_aux_loss_matches_oracle(dtype):
     ids, _, probs = O.top_k_gate(logits.double().cpu().numpy(), E, k)
     want = O.load_balance_loss(ids, probs, E, k)
     assert abs(got - want) <= 1e-5 * want
+
+
+def _nan_inf_rows(E, rng):
+    """Logit rows numpy's stable argsort orders specially: NaN last, -inf before
+    NaN, +-0 ties, a single finite value among -inf, all NaN, all -inf."""
+    ninf, nan = -np.inf, np.nan
+    rows = [np.full(E, nan), np.full(E, ninf), np.where(np.arange(E) % 2, ninf, nan)]
+    r = np.full(E, ninf)
+    r[E - 1] = 0.5
+    rows.append(r)
+    r = np.full(E, nan)
+    r[E // 2] = ninf
+    rows.append(r)
+    r = rng.standard_normal(E)
+    r[::3] = nan
+    rows.append(r)
+    r = rng.standard_normal(E)
+    r[1] = np.inf
+    rows.append(r)
+    r = np.zeros(E)
+    r[::2] = -0.0
+    rows.append(r)
+    return np.stack(rows)
+
+
+@pytest.mark.parametrize("E,k", [(4, 1), (4, 2), (8, 2), (128, 2), (300, 1)])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_gate_nan_inf_rows_match_stable_argsort(E, k, dt):
+    """a NaN / -inf row must route like np.argsort(-logits,
+    kind="stable") (gating.py:159-161), never to an index outside [0, E)."""
+    rng = np.random.default_rng(E + k)
+    lg = np.concatenate([_nan_inf_rows(E, rng), rng.standard_normal((40, E))]).astype(dt)
+    cfg = G.GatingConfig(E, k)
+    with np.errstate(invalid="ignore"):
+        want = np.argsort(-lg.astype(np.float64), axis=1, kind="stable")[:, :k]
+    for inp in (lg, torch.from_numpy(lg).cuda()):
+        g = G.top_k_gate(inp, cfg)
+        ids = g.expert_ids.cpu().numpy() if torch.is_tensor(g.expert_ids) else g.expert_ids
+        assert np.array_equal(ids, want)
+        plan = G.build_dispatch_plan(g, cfg, lg.shape[0])
+        s_ref, l_ref, _ = O.build_dispatch_plan(want, E, k, 1.0)
+        slots = plan.slots.cpu().numpy() if torch.is_tensor(plan.slots) else plan.slots
+        assert np.array_equal(slots, s_ref)
+
+
+@pytest.mark.parametrize("E,k", [(8, 1), (8, 2), (128, 1), (128, 2), (33, 2)])
+def test_fused_gate_nan_rows(E, k):
+    """The tcgen05 gate epilogue: tokens whose logits are NaN / +-inf (NaN or
+    inf activations) route like the stable argsort of the logits it emitted."""
+    from paper_2201_05596_b200 import arch as A
+
+    S, M = 700, 64
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=G.GatingConfig(E, k, 1.0))
+    p = A.init_layer_params(spec, np.random.default_rng(E))
+    layer = A.MoeLayer(spec, p, dtype=torch.bfloat16)
+    x = torch.randn(S, M, device="cuda").to(torch.bfloat16)
+    x[3] = float("nan")
+    x[130, 5] = float("nan")
+    x[131, 0] = float("inf")
+    x[260] = float("-inf")
+    x[261, :8] = float("inf")
+    logits = torch.empty(S, E, device="cuda")
+    layer(x, logits_out=logits)
+    torch.cuda.synchronize()
+    lg = logits.double().cpu().numpy()
+    assert np.isnan(lg[3]).all()
+    with np.errstate(invalid="ignore"):
+        want = np.argsort(-lg, axis=1, kind="stable")[:, :k]
+    ids, gp, slots, load, cap = layer.plan(S)
+    assert np.array_equal(ids.cpu().numpy(), want)
+    s_ref, l_ref, c_ref = O.build_dispatch_plan(want, E, k, 1.0)
+    assert np.array_equal(slots.cpu().numpy(), s_ref)
+    assert np.array_equal(load.cpu().numpy(), l_ref)
+
+
+def test_plan_hand_built_ids():
+    """a hand-built gate may hold ids outside [0, E) (they match no
+    expert's indicator and stay DROPPED, gating.py:229-230) or repeat an
+    expert within a token's k=2 choices (token-major: slots s and s+1)."""
+    rng = np.random.default_rng(5)
+    for k in (1, 2):
+        E, S = 6, 300
+        ids = rng.integers(-2, E + 2, size=(S, k)).astype(np.int64)
+        ids[::7, :] = 3  # repeated choice (k=2) / hot expert
+        ids[5, 0] = 2 ** 33 + 1  # would alias to 1 if narrowed to int32
+        gate = G.TopKGate(expert_ids=ids, gate_probs=np.full((S, k), 0.5),
+                          probs=np.full((S, E), 1.0 / E))
+        cfg = G.GatingConfig(E, k, 1.5)
+        s_ref, l_ref, c_ref = O.build_dispatch_plan(ids, E, k, 1.5)
+        for g in (gate, G.TopKGate(torch.from_numpy(ids).cuda(), torch.full((S, k), 0.5).cuda(),
+                                   torch.full((S, E), 1.0 / E).cuda())):
+            plan = G.build_dispatch_plan(g, cfg, S)
+            slots = plan.slots.cpu().numpy() if torch.is_tensor(plan.slots) else plan.slots
+            load = (plan.expert_load.cpu().numpy() if torch.is_tensor(plan.expert_load)
+                    else plan.expert_load)
+            assert plan.capacity == c_ref
+            assert np.array_equal(slots, s_ref), k
+            assert np.array_equal(load, l_ref), k
