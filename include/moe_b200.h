@@ -190,6 +190,29 @@ int moe_grouped_gemm_bf16_gather(const void* X, int64_t x_rows, const int32_t* r
                                  int64_t rows_const, int64_t max_group_rows, int act,
                                  void* stream);
 
+/* Residual-MoE / PR-MoE layer (arch.py:389-391) with the shared MLP run as extra
+ * groups of the expert launches. Groups are row_stride rows apart: groups
+ * [0, E) are the experts (expert buffer rows, row_stride = capacity), groups
+ * [E, G) the shared MLP over token blocks of row_stride rows (weight_idx E).
+ *  mode 1 (GEMM1, bias + tanh-GELU, forward_ffn's first half arch.py:368-369):
+ *    groups >= a2_group read their A rows from A2 (x) at row
+ *    (g - a2_group) * row_stride + r instead of A (the dispatched buffer).
+ *    D = (G * row_stride, N) bf16; rows past rows[g] are scratch.
+ *  mode 0 (GEMM2): groups < rc_group store y = A @ B_w^T + bias_w to D (expert
+ *    rows); groups >= rc_group (token t = (g - rc_group) * row_stride + r) emit
+ *      out[t] = (x[t] + sum_j gate_probs[t, j] * y[ids[t, j] * cap + slots[t, j]])
+ *               + (A[row] @ B_E^T + bias_E)
+ *    over the kept choices in ascending expert order (forward_layer's order,
+ *    arch.py:399-410), once every expert tile of the launch has stored its y.
+ *  rows: (G) int32 device rows per group; weight_idx: (G) int32; bias (W, N). */
+int moe_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int64_t a2_rows,
+                           int a2_group, int K, const void* B, int64_t b_rows, int N,
+                           const float* bias, void* D, int num_groups, int64_t row_stride,
+                           const int32_t* rows, const int32_t* weight_idx, int64_t max_group_rows,
+                           int mode, int rc_group, const int32_t* ids, const int32_t* slots,
+                           const float* gate_probs, int k, int64_t cap, const void* x, void* out,
+                           int64_t S, void* stream);
+
 /* GEMM2 of a k=1 layer with combine_tokens and the residual add fused into the
  * epilogue (gating.py:281-307, arch.py:389): for every expert-buffer row r
  *   out[row_token[r]] = x_resid[row_token[r]] + row_prob[r] * (A[r] @ B_w^T + bias_w)

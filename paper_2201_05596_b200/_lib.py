@@ -82,6 +82,8 @@ SIGNATURES = {
     "moe_gemm_bf16_wgrad_f32": (_I, [_P, _L, _I, _P, _I, _P, _P]),
     "moe_bwd_dx_bf16": (_I, [_P, _P, _L, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
     "moe_grouped_gemm_f32": (_I, [_P, _I, _P, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L, _I, _P]),
+    "moe_residual_gemm_bf16": (_I, [_P, _L, _P, _L, _I, _I, _P, _L, _I, _P, _P, _I, _L, _P, _P, _L,
+                                    _I, _I, _P, _P, _P, _I, _L, _P, _P, _L, _P]),
 }
 
 _lib = None

@@ -264,6 +264,21 @@ class MoeLayer:
                        if (spec.residual and params.shared is not None) else None)
         if spec.residual and params.shared is None:
             raise ValidationError("residual layer needs shared MLP params")
+        # bf16 Residual-MoE: the shared MLP runs as extra groups (weight index E) of the
+        # expert GEMM launches and its GEMM2 epilogue does the combine + both residual
+        # adds (moe_residual_gemm_bf16); the expert and shared weights live in one
+        # stacked buffer, the DenseFfn / per-expert tensors are views into it
+        self.grouped_shared = self.dtype == torch.bfloat16 and self.shared is not None
+        if self.grouped_shared:
+            sh = self.shared
+            self.w1_all = torch.cat([self.w1, sh.w1]).contiguous()
+            self.w2_all = torch.cat([self.w2, sh.w2]).contiguous()
+            self.b1_all = torch.cat([self.b1, sh.b1]).contiguous()
+            self.b2_all = torch.cat([self.b2, sh.b2]).contiguous()
+            self.w1, self.w2 = self.w1_all[:E * F], self.w2_all[:E * M]
+            self.b1, self.b2 = self.b1_all[:E], self.b2_all[:E]
+            sh.w1, sh.w2 = self.w1_all[E * F:], self.w2_all[E * M:]
+            sh.b1, sh.b2 = self.b1_all[E:], self.b2_all[E:]
         # k=1 bf16 layers without a shared MLP fold combine + residual into GEMM2
         self.fused_combine = bool(fuse_combine and self.dtype == torch.bfloat16 and
                                   self.k == 1 and self.shared is None)
@@ -287,8 +302,12 @@ class MoeLayer:
         cap = self.spec.gating.capacity(S)
         T = (S + _lib.ROUTE_TILE - 1) // _lib.ROUTE_TILE
         i32 = dict(dtype=torch.int32, device=dev)
+        # shared MLP grouped with the experts: its S tokens as ceil(S/cap) groups of
+        # cap rows (needs groups of at least one 128-row tile and <= 2048 groups)
+        nsh = -(-S // cap) if cap else 0
+        grouped = bool(self.grouped_shared and cap >= 128 and E + nsh <= 2048)
         ws = dict(
-            cap=cap, T=T,
+            cap=cap, T=T, grouped_shared=grouped,
             ids=torch.empty((S, k), **i32), slots=torch.empty((S, k), **i32),
             local_rank=torch.empty((S, k), **i32),
             gp=torch.empty((S, k), dtype=torch.float32, device=dev),
@@ -307,7 +326,14 @@ class MoeLayer:
         if self.fused_combine:
             ws["row_token"] = torch.empty(max(E * cap, 1), **i32)
             ws["row_prob"] = torch.empty(max(E * cap, 1), dtype=torch.float32, device=dev)
-        if self.shared is not None:
+        if grouped:
+            G = E + nsh
+            rows_all = torch.empty(G, **i32)
+            rows_all[E:] = torch.tensor([min(cap, S - j * cap) for j in range(nsh)], **i32)
+            ws.update(G=G, rows_all=rows_all, load=rows_all[:E],
+                      widx=torch.tensor(list(range(E)) + [E] * nsh, **i32),
+                      h=torch.empty((G * cap, F), dtype=dt, device=dev))
+        elif self.shared is not None:
             ws["hs"] = torch.empty((S, F), dtype=dt, device=dev)
             ws["ys"] = torch.empty((S, M), dtype=dt, device=dev)
         self._ws[S] = ws
@@ -429,6 +455,22 @@ class MoeLayer:
         _lib.call("moe_dispatch", x.data_ptr(), S, M * x.element_size(), E, k, cap, ids.data_ptr(),
                   lr.data_ptr(), ws["tile_offsets"].data_ptr(), ws["slots"].data_ptr(),
                   ws["xbuf"].data_ptr(), st)
+        if ws["grouped_shared"]:
+            G = ws["G"]
+            ph("gemm1")  # experts + shared MLP (x rows) in one launch, bias + GELU
+            _lib.call("moe_residual_gemm_bf16", ws["xbuf"].data_ptr(), E * cap, x.data_ptr(), S, E,
+                      M, self.w1_all.data_ptr(), (E + 1) * F, F, self.b1_all.data_ptr(),
+                      ws["h"].data_ptr(), G, cap, ws["rows_all"].data_ptr(),
+                      ws["widx"].data_ptr(), cap, 1, 0, None, None, None, k, cap, None, None, S,
+                      st)
+            ph("gemm2")  # experts -> y; shared groups: (x + sum p*y) + shared MLP -> out
+            _lib.call("moe_residual_gemm_bf16", ws["h"].data_ptr(), G * cap, None, 0, 0, F,
+                      self.w2_all.data_ptr(), (E + 1) * M, M, self.b2_all.data_ptr(),
+                      ws["y"].data_ptr(), G, cap, ws["rows_all"].data_ptr(),
+                      ws["widx"].data_ptr(), cap, 0, E, ids.data_ptr(), ws["slots"].data_ptr(),
+                      gp.data_ptr(), k, cap, x.data_ptr(), out.data_ptr(), S, st)
+            ph(None)
+            return out
         if cap > 0:
             ph("gemm1")
             _grouped_gemm(self.dtype, ws["xbuf"], E * cap, M, self.w1, F, self.b1, ws["h"], E,

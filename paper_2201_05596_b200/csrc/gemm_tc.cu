@@ -36,8 +36,16 @@ namespace moe {
 //   EPI_WGRAD    : D[g] (P x N, bf16) = X_g^T Y_g, X_g / Y_g the first k_rows[g] rows
 //                  of group g (rows [g*k_stride, +k_rows[g]) of X and Y)
 //   EPI_WGRAD_ACC: Dacc (P x N, fp32) += X_g^T Y_g for every g (split-K over groups)
+// Residual-MoE layer (arch.py:389-391) as ONE launch per GEMM: the shared MLP runs
+// as extra groups of the expert launches (its tokens split into row_stride-row
+// groups, weight index E):
+//   GEMM1: groups >= a2_group read their A rows from a second matrix (map_a2 = x)
+//   EPI_BIAS_RESID (GEMM2): groups < rc_group are experts, D = acc + b2 (the expert
+//     outputs y); groups >= rc_group are the shared MLP, whose epilogue waits until
+//     every expert tile has stored (device counter) and emits
+//     out[t] = (x[t] + sum_j p_j y[e_j*cap + slot_j]) + (acc + b2_shared).
 enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2, EPI_BIAS_COMBINE = 3, EPI_GELU_SAVE = 4,
-       EPI_GELU_BWD = 5, EPI_WGRAD = 6, EPI_WGRAD_ACC = 7 };
+       EPI_GELU_BWD = 5, EPI_WGRAD = 6, EPI_WGRAD_ACC = 7, EPI_BIAS_RESID = 8 };
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
@@ -95,6 +103,16 @@ struct GemmArgs {
   // through TMA tile::gather4 (map_a is then a {64, 1}-box map over X): the dispatch
   // copy of the k=1 layer is folded into GEMM1's producer
   const int32_t* a_gather;
+  // Residual-MoE shared-MLP groups (see EPI_BIAS_RESID); zero-initialised = off
+  int has_a2, a2_group;       // groups >= a2_group: A rows from map_a2, row (g-a2_group)*row_stride+r
+  int has_rc, rc_group;       // groups >= rc_group: resid-combine epilogue, token rows as for A2
+  const int32_t* c_ids;       // [S, k] routing of the combine
+  const int32_t* c_slots;     // [S, k]
+  const float* c_gp;          // [S, k]
+  int c_k;
+  int64_t c_cap;
+  int64_t c_tokens;           // S
+  int* c_done;                // zeroed: expert-tile epilogue warps done storing y
   int tma_store;    // EPI_BIAS / EPI_BIAS_GELU: whole-box TMA stores through map_d
   int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
   int raster;       // tile order (see tile_at)
@@ -152,7 +170,8 @@ constexpr int out_bufs() {
 }
 template <int EPI, int EW, int CG, int BN = 256>
 constexpr int out_stage_bytes() {
-  return (EPI == EPI_WGRAD || (CG == 2 && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU)))
+  return (EPI == EPI_WGRAD ||
+          (CG == 2 && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID)))
              ? EW * out_bufs<BN>() * 2048 : 0;
 }
 
@@ -165,7 +184,8 @@ template <int BN, int STAGES, int EPI, int CG, int EW, int CL = CG, int SUB = 1>
 __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
-                        const __grid_constant__ CUtensorMap map_d, GemmArgs args) {
+                        const __grid_constant__ CUtensorMap map_d, GemmArgs args,
+                        const __grid_constant__ CUtensorMap map_a2) {
   using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>()>;
   constexpr int TM = BM * CG;  // rows per tile
   constexpr int AS = acc_stages<BN>();
@@ -263,6 +283,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
+    if (args.has_a2) tma_prefetch(&map_a2);
     if (EPI == EPI_WGRAD || args.tma_store) tma_prefetch(&map_d);
   }
   tc_fence_before();
@@ -364,7 +385,12 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
       const int mrow = mb * TMC + (int)(pair * SUB + sub) * TM;  // this pair's m-block
-      const int a_row = (int)(rs + (int64_t)mrow + cta * BM);
+      // shared-MLP groups of a Residual-MoE launch read x (map_a2) instead of the
+      // dispatched expert buffer
+      const bool use_a2 = args.has_a2 && g >= args.a2_group;
+      const CUtensorMap* mA = use_a2 ? &map_a2 : &map_a;
+      const int64_t rs_a = use_a2 ? (int64_t)(g - args.a2_group) * args.row_stride : rs;
+      const int a_row = (int)(rs_a + (int64_t)mrow + cta * BM);
       const int b_row = w * args.N + nb * BN + cta * (BN / CG);
       // gather mode: this lane's 4 source rows of the CTA's 128-row A tile (rows past
       // the group's count read row 0: their outputs are padding)
@@ -486,7 +512,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           if constexpr (kNI > 1) {
-            tma_load_2d_cg2(sa, &map_a, &full[stage], kb * BK, a_row);
+            tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
 #pragma unroll
             for (int i = 0; i < kNI; ++i)  // B rows of MMA i: [nb*BN + i*256 + cta*128, +128)
               tma_load_2d_cg2(sb + i * 128 * BK * 2, &map_b, &full[stage], kb * BK,
@@ -498,7 +524,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           } else if constexpr (CL == 4) {
             // weight tile shared by both pairs: load my half of my 128 B rows and
             // multicast it to my counterpart in the other pair (same cta index)
-            tma_load_2d_cg2(sa, &map_a, &full[stage], kb * BK, a_row);
+            tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
             constexpr int kHalf = BN / CG / CLP;  // B rows per multicast box
             tma_load_2d_cg2_mc(sb + pair * kHalf * BK * 2, &map_b, &full[stage], kb * BK,
                                b_row + pair * kHalf, (uint16_t)((1u << cta) | (1u << (cta + 2))));
@@ -507,7 +533,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             else
               mbar_arrive_cluster(&full[stage], pl);
           } else if constexpr (CG == 2) {
-            tma_load_2d_cg2(sa, &map_a, &full[stage], kb * BK, a_row);
+            tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
             tma_load_2d_cg2(sb, &map_b, &full[stage], kb * BK, b_row);
             if (leader)
               mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
@@ -515,7 +541,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               mbar_arrive_cluster(&full[stage], pl);
           } else {
             mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-            tma_load_2d(sa, &map_a, &full[stage], kb * BK, a_row);
+            tma_load_2d(sa, mA, &full[stage], kb * BK, a_row);
             tma_load_2d(sb, &map_b, &full[stage], kb * BK, b_row);
           }
         }
@@ -742,6 +768,41 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         }
         if constexpr (EPI == EPI_GELU_BWD) xrow = args.x_resid + out_row * N;
         if constexpr (EPI == EPI_GELU_SAVE) arow = args.out + out_row * N;
+        // EPI_BIAS_RESID, shared-MLP group: this row is token c_t; its kept expert rows
+        // (ascending expert id, forward_layer's order, arch.py:399-410) and probabilities
+        const bool rc = EPI == EPI_BIAS_RESID && args.has_rc && g >= args.rc_group;
+        int64_t c_t = 0, cr0 = 0, cr1 = 0;
+        float cp0 = 0.f, cp1 = 0.f;
+        int cn = 0;
+        if constexpr (EPI == EPI_BIAS_RESID) {
+          if (rc) {
+            // every expert tile's y must be stored first: the expert tiles precede the
+            // shared ones in tile order and every CTA runs its tiles in order, so they
+            // are all claimed by running CTAs and complete without waiting on this one
+            const int expected = tile_start[args.rc_group] * EW * CG;
+            if (lane == 0) {
+              while (ld_acquire_gpu(args.c_done) < expected) __nanosleep(256);
+            }
+            __syncwarp();
+            c_t = (int64_t)(g - args.rc_group) * args.row_stride + local_row;
+            if (valid) {
+              int e0 = 0;
+              for (int j = 0; j < args.c_k; ++j) {
+                const int sl = args.c_slots[c_t * args.c_k + j];
+                if (sl < 0) continue;
+                const int e = args.c_ids[c_t * args.c_k + j];
+                const int64_t r = (int64_t)e * args.c_cap + sl;
+                const float pj = args.c_gp[c_t * args.c_k + j];
+                if (cn == 0) { cr0 = r; cp0 = pj; e0 = e; }
+                else if (e < e0) { cr1 = cr0; cp1 = cp0; cr0 = r; cp0 = pj; }
+                else { cr1 = r; cp1 = pj; }
+                ++cn;
+              }
+            }
+            drow = args.out + c_t * N;
+            xrow = args.x_resid + c_t * N;
+          }
+        }
         constexpr bool kLoadX = EPI == EPI_BIAS_COMBINE || EPI == EPI_GELU_BWD;
         // residual row chunks (COMBINE) are prefetched one chunk ahead
         auto load_x = [&](int c, uint4 (&xq)[4]) {
@@ -835,6 +896,57 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             v[4 * q + 1] = fmaf(__uint_as_float(r[c % kRB][4 * q + 1]), sc, bq.y);
             v[4 * q + 2] = fmaf(__uint_as_float(r[c % kRB][4 * q + 2]), sc, bq.z);
             v[4 * q + 3] = fmaf(__uint_as_float(r[c % kRB][4 * q + 3]), sc, bq.w);
+          }
+          if constexpr (EPI == EPI_BIAS_RESID) {
+            if (rc) {  // out[t] = (x[t] + sum_j p_j y_j) + (acc + b2), arch.py:389-391
+              if (!valid) continue;
+              const __nv_bfloat16* y0r = args.D + cr0 * N;
+              const __nv_bfloat16* y1r = args.D + cr1 * N;
+              if (vec_ok && col0 + 32 <= N) {
+                uint4 xq[4], aq[4], bq[4];
+                const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  xq[q] = __ldg(reinterpret_cast<const uint4*>(xrow + col0) + q);
+                  // y was stored by this launch's expert tiles: L2-coherent loads
+                  aq[q] = cn > 0 ? __ldcg(reinterpret_cast<const uint4*>(y0r + col0) + q) : z4;
+                  bq[q] = cn > 1 ? __ldcg(reinterpret_cast<const uint4*>(y1r + col0) + q) : z4;
+                }
+                const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(xq);
+                const __nv_bfloat16* ab = reinterpret_cast<const __nv_bfloat16*>(aq);
+                const __nv_bfloat16* bb = reinterpret_cast<const __nv_bfloat16*>(bq);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  float acc_m = 0.f;  // the zero accumulator of scatter_rows
+                  if (cn > 0) acc_m = __fadd_rn(acc_m, __fmul_rn(cp0, __bfloat162float(ab[i])));
+                  if (cn > 1) acc_m = __fadd_rn(acc_m, __fmul_rn(cp1, __bfloat162float(bb[i])));
+                  v[i] = __fadd_rn(__fadd_rn(__bfloat162float(xb[i]), acc_m), v[i]);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(drow + col0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  uint4 pk;
+                  pk.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                  pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                  pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                  pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                  if (args.stream_hint)
+                    st_global_hint(dst + q, pk, pol_stream);
+                  else
+                    dst[q] = pk;
+                }
+              } else {
+                for (int i = 0; i < 32; ++i) {
+                  if (col0 + i >= N) break;
+                  float acc_m = 0.f;
+                  if (cn > 0) acc_m = __fadd_rn(acc_m, __fmul_rn(cp0, __bfloat162float(__ldcg(y0r + col0 + i))));
+                  if (cn > 1) acc_m = __fadd_rn(acc_m, __fmul_rn(cp1, __bfloat162float(__ldcg(y1r + col0 + i))));
+                  drow[col0 + i] = __float2bfloat16_rn(
+                      __fadd_rn(__fadd_rn(__bfloat162float(xrow[col0 + i]), acc_m), v[i]));
+                }
+              }
+              continue;
+            }
           }
           if constexpr (EPI == EPI_WGRAD_ACC) {  // split-K partial: fp32 reduction in HBM/L2
             if (kzero) continue;
@@ -964,6 +1076,20 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               mbar_arrive_cluster(&tempty[acc], pl);  // the leader's MMA reuses it
             else
               mbar_arrive(&tempty[acc]);
+          }
+        }
+        if constexpr (EPI == EPI_BIAS_RESID) {
+          if (args.has_rc && !rc) {
+            // expert tile: publish this warp's y stores to the shared-MLP epilogues
+            // (bulk TMA stores complete -> async-proxy writes ordered before the release)
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) {
+              bulk_wait_group_all();
+              fence_proxy_async_global();
+              red_release_gpu_add(args.c_done, 1);
+            }
+            __syncwarp();
           }
         }
       } else {
@@ -1365,8 +1491,9 @@ static cudaError_t ensure_smem_attr(Kern kern, int bytes, std::atomic<uint64_t>&
 template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4, int CL = CG, int SUB = 1>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
                      int64_t max_tiles, cudaStream_t st, const CUtensorMap* md = nullptr,
-                     int64_t grid_cap = 0) {
+                     int64_t grid_cap = 0, const CUtensorMap* ma2 = nullptr) {
   using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>()>;
+  static_assert(L::kTotal <= 227 * 1024, "dynamic shared memory beyond the 227 KB per CTA");
   auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW, CL, SUB>;
   static std::atomic<uint64_t> attr_done{0};
   {
@@ -1405,7 +1532,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
     if (grid > (int64_t)max_clusters * CL) grid = (int64_t)max_clusters * CL;
     cfg.gridDim = dim3((unsigned)grid);
   }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, md ? *md : mb, args);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, md ? *md : mb, args, ma2 ? *ma2 : ma);
   return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
@@ -1654,6 +1781,105 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                   : launch_tc<256, 4, EPI_BIAS, 1, 4>(ma, mb, a, max_tiles, st);
   }
 #undef MOE_TC
+}
+
+// Residual-MoE layer GEMMs with the shared MLP as extra groups (see EPI_BIAS_RESID):
+//   mode 1 (GEMM1): bias + GELU; groups >= a2_group read A rows from A2 (= x)
+//   mode 0 (GEMM2): groups < rc_group store y = acc + b2 to D; groups >= rc_group
+//                   combine into out (token rows), after every expert tile stored
+// Groups are row_stride rows apart (expert buffers: row_stride = capacity; the
+// shared groups split the tokens into row_stride-row blocks).
+int launch_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int64_t a2_rows,
+                              int a2_group, int K, const void* B, int64_t b_rows, int N,
+                              const float* bias, void* D, int G, int64_t row_stride,
+                              const int32_t* rows, const int32_t* weight_idx,
+                              int64_t max_group_rows, int mode, int rc_group, const int32_t* ids,
+                              const int32_t* slots, const float* gp, int k, int64_t cap,
+                              const void* x, void* out, int64_t S, cudaStream_t st) {
+  if (G < 1 || G > kMaxGroups || K < 8 || (K % 8) || N < 8 || (N % 8) || row_stride < 1)
+    return MOE_EINVAL;
+  static const int stream_hint = [] {
+    const char* v = getenv("MOE_STORE_HINT");
+    return v ? atoi(v) : 1;
+  }();
+  int BN = 256;
+  if (N <= 32) BN = 32;
+  else if (N <= 64) BN = 64;
+  else if (N <= 128) BN = 128;
+  const int CG = (BN == 256 && max_group_rows > BM) ? 2 : 1;
+  CUtensorMap ma, mb, ma2, md;
+  int rc = make_map(&ma, A, a_rows, K, BM);
+  if (rc) return rc;
+  rc = make_map(&mb, B, b_rows, K, BN / CG);
+  if (rc) return rc;
+  GemmArgs a{};
+  a.bias = bias;
+  a.D = (__nv_bfloat16*)D;
+  a.K = K;
+  a.N = N;
+  a.G = G;
+  a.row_stride = row_stride;
+  a.rows = rows;
+  a.weight_idx = weight_idx;
+  a.stream_hint = stream_hint;
+  const int64_t nblk = (N + BN - 1) / BN;
+  const int64_t tm = (int64_t)BM * CG;
+  const int64_t max_tiles = (int64_t)G * ((max_group_rows + tm - 1) / tm) * nblk;
+  if (max_tiles == 0) return 0;
+  if (mode == 1) {
+    if (A2 == nullptr || a2_group < 0 || a2_group > G) return MOE_EINVAL;
+    rc = make_map(&ma2, A2, a2_rows, K, BM);
+    if (rc) return rc;
+    a.has_a2 = 1;
+    a.a2_group = a2_group;
+    a.tile_counter = dyn_counter(st, K, N);
+    if (CG == 2) {
+      rc = make_map_out3d(&md, D, G, row_stride, N);
+      if (rc) return rc;
+      a.tma_store = 1;
+      return launch_tc<256, MOE_FWD_STAGES, EPI_BIAS_GELU, 2, MOE_FWD_EW>(ma, mb, a, max_tiles, st,
+                                                                          &md, 0, &ma2);
+    }
+    switch (BN) {
+      case 32: return launch_tc<32, 8, EPI_BIAS_GELU, 1, 4>(ma, mb, a, max_tiles, st, nullptr, 0, &ma2);
+      case 64: return launch_tc<64, 8, EPI_BIAS_GELU, 1, 8>(ma, mb, a, max_tiles, st, nullptr, 0, &ma2);
+      case 128: return launch_tc<128, 6, EPI_BIAS_GELU, 1, 8>(ma, mb, a, max_tiles, st, nullptr, 0, &ma2);
+      default: return launch_tc<256, 4, EPI_BIAS_GELU, 1, 4>(ma, mb, a, max_tiles, st, nullptr, 0, &ma2);
+    }
+  }
+  if (mode != 0 || rc_group < 0 || rc_group > G || ids == nullptr || slots == nullptr ||
+      gp == nullptr || x == nullptr || out == nullptr || k < 1 || k > 2)
+    return MOE_EINVAL;
+  a.has_rc = 1;
+  a.rc_group = rc_group;
+  a.c_ids = ids;
+  a.c_slots = slots;
+  a.c_gp = gp;
+  a.c_k = k;
+  a.c_cap = cap;
+  a.c_tokens = S;
+  a.x_resid = (const __nv_bfloat16*)x;
+  a.out = (__nv_bfloat16*)out;
+  // the completion counter: a zeroed slot of the per-device pool (graph-safe)
+  a.c_done = dyn_counter(st, 0, 0, true);
+  if (a.c_done == nullptr) return MOE_EINVAL;
+  a.tile_counter = dyn_counter(st, K, N);
+  if (CG == 2) {
+    if (rc_group > 0) {
+      rc = make_map_out3d(&md, D, rc_group, row_stride, N);
+      if (rc) return rc;
+      a.tma_store = 1;
+    }
+    // 5 stages: with the 32 KB TMA-store staging, 6 would exceed 227 KB of smem
+    return launch_tc<256, 5, EPI_BIAS_RESID, 2, 8>(ma, mb, a, max_tiles, st,
+                                                   rc_group > 0 ? &md : nullptr);
+  }
+  switch (BN) {
+    case 32: return launch_tc<32, 8, EPI_BIAS_RESID, 1, 4>(ma, mb, a, max_tiles, st);
+    case 64: return launch_tc<64, 8, EPI_BIAS_RESID, 1, 8>(ma, mb, a, max_tiles, st);
+    case 128: return launch_tc<128, 6, EPI_BIAS_RESID, 1, 8>(ma, mb, a, max_tiles, st);
+    default: return launch_tc<256, 4, EPI_BIAS_RESID, 1, 4>(ma, mb, a, max_tiles, st);
+  }
 }
 
 // Weight gradients: D = X^T Y per group (see EPI_WGRAD). X: [x_rows, P], Y:

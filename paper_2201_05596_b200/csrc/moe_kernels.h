@@ -62,6 +62,14 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              void* out = nullptr, int x_by_row = 0, int pad_scratch = 0,
                              const int32_t* a_gather = nullptr);
 
+int launch_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int64_t a2_rows,
+                              int a2_group, int K, const void* B, int64_t b_rows, int N,
+                              const float* bias, void* D, int G, int64_t row_stride,
+                              const int32_t* rows, const int32_t* weight_idx,
+                              int64_t max_group_rows, int mode, int rc_group, const int32_t* ids,
+                              const int32_t* slots, const float* gp, int k, int64_t cap,
+                              const void* x, void* out, int64_t S, cudaStream_t st);
+
 int launch_wgrad_bf16(const void* X, int64_t x_rows, int P, const void* Y, int Q, int G,
                       int64_t k_stride, const int32_t* k_rows, int64_t k_rows_const, void* D,
                       int acc, cudaStream_t st);

@@ -11,6 +11,7 @@
 #include "common.cuh"
 #include "moe_kernels.h"
 
+#include <atomic>
 #include <cstdlib>
 
 namespace moe {
@@ -493,6 +494,135 @@ __global__ void combine_kernel(const T* __restrict__ y, int64_t S, int M, int k,
   }
 }
 
+// Block-staged combine (16-B vector path): a block owns TB consecutive tokens.
+// Its first TB threads resolve the tokens' routing (ids / slots / row_index / gp
+// -> up to two (row, prob) pairs in summation order) into shared memory in one
+// coalesced pass, so combine_kernel's per-token index -> row -> data chain
+// collapses into one round trip per block; then each warp streams whole rows,
+// all U 16-B loads of every input row issued before any is consumed. Same
+// arithmetic in the same order as combine_kernel.
+template <typename T>
+struct Vec16 {
+  static constexpr int N = 16 / sizeof(T);
+  MOE_DEV static void unpack(const uint4& u, typename Acc<T>::type (&v)[N]) {
+    const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = to_acc(e[i]);
+  }
+  MOE_DEV static uint4 pack(const typename Acc<T>::type (&v)[N]) {
+    uint4 u;
+    T* e = reinterpret_cast<T*>(&u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if constexpr (sizeof(T) == 8) {
+        e[i] = v[i];
+      } else {
+        e[i] = from_acc<T>(v[i]);
+      }
+    }
+    return u;
+  }
+};
+
+template <typename T, typename P, bool kExpertOrder, int TB, int U, bool kShared>
+__global__ void __launch_bounds__(256, 3) combine_tb_kernel(
+    const T* __restrict__ y, int64_t S, int M, int k, int E, int64_t cap,
+    const int32_t* __restrict__ ids, const int32_t* __restrict__ slots,
+    const int32_t* __restrict__ row_index, const P* __restrict__ gp, const T* __restrict__ x,
+    const T* __restrict__ shared, T* __restrict__ out) {
+  using A = typename Acc<T>::type;
+  using W = Vec16<T>;
+  constexpr int NV = W::N;
+  __shared__ int64_t s_r[2][TB];
+  __shared__ A s_p[2][TB];
+  __shared__ int s_n[TB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nv = M / NV;  // 16-B vectors per row
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  // persistent grid (resident blocks only): block b owns the contiguous token range
+  // [b*S/grid, (b+1)*S/grid), so the work is balanced to a token, not to a batch
+  const int64_t lo = (int64_t)blockIdx.x * S / gridDim.x;
+  const int64_t hi = (int64_t)(blockIdx.x + 1) * S / gridDim.x;
+  for (int64_t t0 = lo; t0 < hi; t0 += TB) {
+    if (threadIdx.x < TB && t0 + threadIdx.x < hi) {
+      const int64_t t = t0 + threadIdx.x;
+      int64_t r0 = -1, r1 = -1;
+      A p0 = 0, p1 = 0;
+      int e0 = 0, e1 = 0, n = 0;
+      for (int j = 0; j < k; ++j) {
+        int64_t r;
+        if (row_index != nullptr) {
+          r = row_index[t * k + j];
+        } else {
+          const int sl = slots[t * k + j];
+          r = sl >= 0 ? (int64_t)ids[t * k + j] * cap + sl : -1;
+        }
+        if (r >= 0) {
+          const A pj = (A)gp[t * k + j];
+          const int ej = ids[t * k + j];
+          if (n == 0) { r0 = r; p0 = pj; e0 = ej; }
+          else { r1 = r; p1 = pj; e1 = ej; }
+          ++n;
+        }
+      }
+      if (kExpertOrder && n == 2 && e1 < e0) {
+        int64_t tr = r0; r0 = r1; r1 = tr;
+        A tp = p0; p0 = p1; p1 = tp;
+      }
+      s_r[0][threadIdx.x] = r0;
+      s_r[1][threadIdx.x] = r1;
+      s_p[0][threadIdx.x] = p0;
+      s_p[1][threadIdx.x] = p1;
+      s_n[threadIdx.x] = n;
+    }
+    __syncthreads();
+    for (int i = warp; i < TB && t0 + i < hi; i += nw) {
+      const int64_t t = t0 + i;
+      const int n = s_n[i];
+      const A p0 = s_p[0][i], p1 = s_p[1][i];
+      const uint4* y0 = reinterpret_cast<const uint4*>(y + (n > 0 ? s_r[0][i] : 0) * M);
+      const uint4* y1 = reinterpret_cast<const uint4*>(y + (n > 1 ? s_r[1][i] : 0) * M);
+      const uint4* xv = reinterpret_cast<const uint4*>(x + t * M);
+      const uint4* sv = reinterpret_cast<const uint4*>(shared + t * M);
+      uint4* ov = reinterpret_cast<uint4*>(out + t * M);
+      for (int c0 = 0; c0 < nv; c0 += 32 * U) {
+        uint4 a0[U], a1[U], xa[U], sa[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * 32 + lane;
+          const bool in = c < nv;
+          a0[u] = (in && n > 0) ? __ldcs(y0 + c) : z;
+          a1[u] = (in && n > 1) ? __ldcs(y1 + c) : z;
+          xa[u] = (in && x != nullptr) ? __ldcs(xv + c) : z;
+          if constexpr (kShared) sa[u] = in ? __ldcs(sv + c) : z;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c >= nv) continue;
+          A v0[NV], v1[NV], vx[NV], vs[NV], o[NV];
+          W::unpack(a0[u], v0);
+          W::unpack(a1[u], v1);
+          W::unpack(xa[u], vx);
+          if constexpr (kShared) W::unpack(sa[u], vs);
+#pragma unroll
+          for (int q = 0; q < NV; ++q) {
+            A acc = 0;  // the zero accumulator of scatter_rows / np.add.at
+            if (n > 0) acc = add_rn(acc, mul_rn(p0, v0[q]));
+            if (n > 1) acc = add_rn(acc, mul_rn(p1, v1[q]));
+            A r = acc;
+            if (x != nullptr) r = add_rn(vx[q], acc);
+            if constexpr (kShared) r = add_rn(r, vs[q]);
+            o[q] = r;
+          }
+          __stcs(ov + c, W::pack(o));
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ============================================================ load-balance loss
 // E * sum_e (count_e / (S k)) * (mean_t probs[t, e]) with pre-drop counts
 // (arch.py:297-313). Statistics in float64.
@@ -667,6 +797,27 @@ int launch_scatter(const ScatterArgs& args, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
+// Resident blocks of a kernel on the current device (persistent grids), cached
+// per (kernel instance, device ordinal).
+template <typename Kern>
+static int64_t resident_blocks(Kern kern, int threads) {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    int per_sm = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1)
+      sms = 148;
+    v = per_sm * sms;
+    cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 template <typename T, typename P, int VEC>
 static void combine_vec(bool expert_order, int g, int threads, cudaStream_t st, const void* y,
                         int64_t S, int M, int k, int E, int64_t cap, const int32_t* ids,
@@ -674,8 +825,41 @@ static void combine_vec(bool expert_order, int g, int threads, cudaStream_t st, 
                         const void* x, const void* shared, void* out) {
   static const int tpw = [] {
     const char* v = getenv("MOE_COMBINE_TPW");
-    return v ? atoi(v) : 2;
+    return v ? atoi(v) : 0;
   }();
+  // default (MOE_COMBINE_TPW unset / 0): the block-staged kernel, 32 tokens per
+  // 256-thread block; MOE_COMBINE_TB=16 halves the block's token batch
+  static const int tb = [] {
+    const char* v = getenv("MOE_COMBINE_TB");
+    return v ? atoi(v) : 32;
+  }();
+  if (tpw == 0 && VEC > 1) {
+    const int64_t blocks = (S + tb - 1) / tb;
+#define MOE_COMBINE_TB(TB_, EO_, SH_)                                                           \
+  {                                                                                             \
+    auto kern = combine_tb_kernel<T, P, EO_, TB_, (sizeof(T) == 2 ? 2 : 4), SH_>;               \
+    const int64_t res = resident_blocks(kern, 256);                                             \
+    const int gb = (int)(blocks < res ? blocks : res);                                          \
+    kern<<<gb, 256, 0, st>>>((const T*)y, S, M, k, E, cap, ids, slots, row_index, (const P*)gp, \
+                             (const T*)x, (const T*)shared, (T*)out);                           \
+  }
+    const bool sh = shared != nullptr;
+    if (tb == 16) {
+      if (expert_order) {
+        if (sh) MOE_COMBINE_TB(16, true, true) else MOE_COMBINE_TB(16, true, false)
+      } else {
+        if (sh) MOE_COMBINE_TB(16, false, true) else MOE_COMBINE_TB(16, false, false)
+      }
+    } else {
+      if (expert_order) {
+        if (sh) MOE_COMBINE_TB(32, true, true) else MOE_COMBINE_TB(32, true, false)
+      } else {
+        if (sh) MOE_COMBINE_TB(32, false, true) else MOE_COMBINE_TB(32, false, false)
+      }
+    }
+#undef MOE_COMBINE_TB
+    return;
+  }
   if (tpw == 4 && VEC > 1) {
     const int g4 = (g + 3) / 4;
     if (expert_order)

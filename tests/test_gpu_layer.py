@@ -220,6 +220,8 @@ def test_fused_combine_matches_unfused():
     (16384, 1024, 32, 1, 1.0, True, 0.5, [0, 7, 31]),     # config 4, PR-MoE-32 layer
     (16384, 1024, 64, 1, 1.0, True, 0.0, [1, 40]),        # config 4, PR-MoE-64 layer
     (2000, 256, 8, 2, 0.7, True, 1.0, list(range(8))),    # ragged S, heavy drops
+    (4096, 256, 64, 1, 1.0, True, 0.5, list(range(64))),  # cap 64: shared MLP not grouped
+    (3001, 512, 4, 2, 1.1, True, 0.0, list(range(4))),    # grouped, ragged last shared group
 ])
 def test_bf16_layers_sampled(cfg):
     S, M, E, k, cf, res, skew, subset = cfg
