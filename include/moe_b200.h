@@ -204,14 +204,18 @@ int moe_grouped_gemm_bf16_gather(const void* X, int64_t x_rows, const int32_t* r
  *               + (A[row] @ B_E^T + bias_E)
  *    over the kept choices in ascending expert order (forward_layer's order,
  *    arch.py:399-410), once every expert tile of the launch has stored its y.
- *  rows: (G) int32 device rows per group; weight_idx: (G) int32; bias (W, N). */
+ *  rows: (G) int32 device rows per group; weight_idx: (G) int32; bias (W, N).
+ *  row_index (nullable, (S, k)): the y row of each choice (-1 = dropped) instead
+ *    of ids * cap + slots - the expert-parallel source side, whose expert rows
+ *    came back over NVLink into a (S * k)-row return buffer passed as D with
+ *    rc_group = 0. */
 int moe_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int64_t a2_rows,
                            int a2_group, int K, const void* B, int64_t b_rows, int N,
                            const float* bias, void* D, int num_groups, int64_t row_stride,
                            const int32_t* rows, const int32_t* weight_idx, int64_t max_group_rows,
                            int mode, int rc_group, const int32_t* ids, const int32_t* slots,
                            const float* gate_probs, int k, int64_t cap, const void* x, void* out,
-                           int64_t S, void* stream);
+                           int64_t S, const int32_t* row_index, void* stream);
 
 /* GEMM2 of a k=1 layer with combine_tokens and the residual add fused into the
  * epilogue (gating.py:281-307, arch.py:389): for every expert-buffer row r
@@ -349,13 +353,31 @@ int moe_ipc_allgather_i32(const int32_t* src, int n, int32_t* const* peer_dst, i
  * row_base[e] + slot - slot_base[e], with its token index and gate
  * probability to peer_token / peer_prob (device arrays of world pointers);
  * row_index (S, k) gets that owner-side row (or -1). Fully dropped tokens:
- * out_dropped[t] = x[t] (local). */
+ * out_dropped[t] = x[t] (local; nullable). peer_src (nullable; device array of
+ * world int32 pointers) selects the push return: each receive row also records
+ * its source (my_rank) and return row t*k + j (in peer_token), and row_index
+ * gets the return row t*k + j instead of the owner-side row. */
 int moe_dispatch_p2p(const void* x, int64_t S, int64_t row_bytes, int E, int k, int64_t cap,
                      const int32_t* ids, const int32_t* local_rank, const int32_t* tile_offsets,
                      const float* gate_probs, const int32_t* slot_base, const int32_t* row_base,
                      int e_per_rank, void* const* peer_recv, int32_t* const* peer_token,
                      float* const* peer_prob, int32_t* slots, int32_t* row_index,
-                     void* out_dropped, void* stream);
+                     void* out_dropped, int32_t* const* peer_src, int my_rank, void* stream);
+
+/* Owner side of the push return (any k, Residual-MoE included): GEMM2 over the
+ * receive buffer, every valid row r stored straight back over NVLink to rank
+ * row_src[r]'s buffer push_base[row_src[r]] at row row_token[r]:
+ *  combine = 1 (k = 1 layers): the combined row x_r + row_prob[r] * (acc + b2)
+ *    (x_r = x_rows[r], the dispatched token row), into the source's output;
+ *  combine = 0: y = acc + b2, into the source's (S * k)-row return buffer, which
+ *    the source then combines locally (moe_combine / moe_residual_gemm_bf16).
+ * row_token / row_src / row_prob come from moe_dispatch_p2p with peer_src set. */
+int moe_grouped_gemm_bf16_push(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
+                               int N, const float* bias, int num_groups, const int32_t* row_start,
+                               const int32_t* rows, const int32_t* weight_idx,
+                               int64_t max_group_rows, int combine, const int32_t* row_token,
+                               const float* row_prob, const int32_t* row_src,
+                               void* const* push_base, const void* x_rows, void* stream);
 
 /* Owner side of a k=1 EP layer: GEMM2 + combine + residual, in the receive
  * layout: out_rows[r] = x_rows[r] + row_prob[r] * (A[r] @ B_w^T + b_w), with

@@ -64,7 +64,9 @@ SIGNATURES = {
     "moe_ipc_barrier": (_I, [_P, _P, _I, _I, _P, _P, _P]),
     "moe_ipc_allgather_i32": (_I, [_P, _I, _P, _I, _I, _P, _P, _P, _P, _P]),
     "moe_dispatch_p2p": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P,
-                              _P, _P, _P]),
+                              _P, _P, _P, _I, _P]),
+    "moe_grouped_gemm_bf16_push": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _P, _P, _L, _I, _P,
+                                        _P, _P, _P, _P, _P]),
     "moe_grouped_gemm_bf16_combine_rows": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _P, _P, _L,
                                                 _P, _P, _P, _P, _P]),
     "moe_pull_rows_p2p": (_I, [_L, _L, _I, _I, _P, _P, _I, _P, _P, _P]),
@@ -83,7 +85,7 @@ SIGNATURES = {
     "moe_bwd_dx_bf16": (_I, [_P, _P, _L, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
     "moe_grouped_gemm_f32": (_I, [_P, _I, _P, _I, _P, _P, _I, _P, _L, _P, _L, _P, _L, _I, _P]),
     "moe_residual_gemm_bf16": (_I, [_P, _L, _P, _L, _I, _I, _P, _L, _I, _P, _P, _I, _L, _P, _P, _L,
-                                    _I, _I, _P, _P, _P, _I, _L, _P, _P, _L, _P]),
+                                    _I, _I, _P, _P, _P, _I, _L, _P, _P, _L, _P, _P]),
 }
 
 _lib = None

@@ -335,7 +335,11 @@ class MoeLayer:
                       h=torch.empty((G * cap, F), dtype=dt, device=dev))
         elif self.shared is not None:
             ws["hs"] = torch.empty((S, F), dtype=dt, device=dev)
-            ws["ys"] = torch.empty((S, M), dtype=dt, device=dev)
+            if dt == torch.float32:
+                ws["ys"] = torch.empty((S, M), dtype=dt, device=dev)
+            else:  # the shared GEMM2 + combine epilogue over one group of S token rows
+                ws["sh_rows"] = torch.tensor([S], **i32)
+                ws["sh_w"] = torch.zeros(1, **i32)
         self._ws[S] = ws
         return ws
 
@@ -462,13 +466,13 @@ class MoeLayer:
                       M, self.w1_all.data_ptr(), (E + 1) * F, F, self.b1_all.data_ptr(),
                       ws["h"].data_ptr(), G, cap, ws["rows_all"].data_ptr(),
                       ws["widx"].data_ptr(), cap, 1, 0, None, None, None, k, cap, None, None, S,
-                      st)
+                      None, st)
             ph("gemm2")  # experts -> y; shared groups: (x + sum p*y) + shared MLP -> out
             _lib.call("moe_residual_gemm_bf16", ws["h"].data_ptr(), G * cap, None, 0, 0, F,
                       self.w2_all.data_ptr(), (E + 1) * M, M, self.b2_all.data_ptr(),
                       ws["y"].data_ptr(), G, cap, ws["rows_all"].data_ptr(),
                       ws["widx"].data_ptr(), cap, 0, E, ids.data_ptr(), ws["slots"].data_ptr(),
-                      gp.data_ptr(), k, cap, x.data_ptr(), out.data_ptr(), S, st)
+                      gp.data_ptr(), k, cap, x.data_ptr(), out.data_ptr(), S, None, st)
             ph(None)
             return out
         if cap > 0:
@@ -479,6 +483,21 @@ class MoeLayer:
             _grouped_gemm(self.dtype, ws["h"], E * cap, F, self.w2, M, self.b2, ws["y"], E, None,
                           cap, ws["load"], 0, cap, _lib.MOE_ACT_NONE, scratch_pad=True)
         shared_out = None
+        if self.shared is not None and self.dtype == torch.bfloat16:
+            # Residual-MoE, shared MLP not grouped (small capacity): shared GEMM1, then
+            # its GEMM2 with the combine + both residual adds in the epilogue, the same
+            # arithmetic as the grouped launch (arch.py:389-391)
+            ph("shared_mlp")
+            sh = self.shared
+            _grouped_gemm(self.dtype, x, S, M, sh.w1, F, sh.b1, ws["hs"], 1, None, 0, None, S, S,
+                          _lib.MOE_ACT_GELU, scratch_pad=True)
+            _lib.call("moe_residual_gemm_bf16", ws["hs"].data_ptr(), S, None, 0, 0, F,
+                      sh.w2.data_ptr(), M, M, sh.b2.data_ptr(), ws["y"].data_ptr(), 1, S,
+                      ws["sh_rows"].data_ptr(), ws["sh_w"].data_ptr(), S, 0, 0, ids.data_ptr(),
+                      ws["slots"].data_ptr(), gp.data_ptr(), k, cap, x.data_ptr(),
+                      out.data_ptr(), S, None, st)
+            ph(None)
+            return out
         if self.shared is not None:
             ph("shared_mlp")
             shared_out = self.shared(x, ws["hs"], ws["ys"])

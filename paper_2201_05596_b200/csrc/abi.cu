@@ -270,7 +270,7 @@ int moe_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int64_
                            const int32_t* rows, const int32_t* weight_idx, int64_t max_group_rows,
                            int mode, int rc_group, const int32_t* ids, const int32_t* slots,
                            const float* gate_probs, int k, int64_t cap, const void* x, void* out,
-                           int64_t S, void* stream) {
+                           int64_t S, const int32_t* row_index, void* stream) {
   CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 8 && N % 8 == 0 && num_groups >= 1);
   CHECK(row_stride >= 1 && max_group_rows >= 0 && max_group_rows <= row_stride);
   CHECK(mode == 0 || mode == 1);
@@ -280,14 +280,15 @@ int moe_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int64_
   if (mode == 1) {
     CHECK(A2 && a2_rows >= 0 && a2_group >= 0 && a2_group <= num_groups);
   } else {
-    CHECK(rc_group >= 0 && rc_group <= num_groups && ids && slots && gate_probs && x && out);
+    CHECK(rc_group >= 0 && rc_group <= num_groups && ids && (slots || row_index) && gate_probs &&
+          x && out);
     CHECK(k == 1 || k == 2);
     CHECK(cap >= 0 && S >= 0);
   }
   return moe::launch_residual_gemm_bf16(A, a_rows, A2, a2_rows, a2_group, K, B, b_rows, N, bias, D,
                                         num_groups, row_stride, rows, weight_idx, max_group_rows,
                                         mode, rc_group, ids, slots, gate_probs, k, cap, x, out, S,
-                                        S_(stream));
+                                        S_(stream), row_index);
 }
 
 int moe_grouped_gemm_f32(const float* A, int K, const float* B, int N, const float* bias, float* D,

@@ -342,7 +342,7 @@ int moe_dispatch_p2p(const void* x, int64_t S, int64_t row_bytes, int E, int k, 
                      const float* gate_probs, const int32_t* slot_base, const int32_t* row_base,
                      int e_per_rank, void* const* peer_recv, int32_t* const* peer_token,
                      float* const* peer_prob, int32_t* slots, int32_t* row_index,
-                     void* out_dropped, void* stream) {
+                     void* out_dropped, int32_t* const* peer_src, int my_rank, void* stream) {
   CHECK(S >= 0 && row_bytes >= 0 && row_bytes % 2 == 0 && E >= 1 && (k == 1 || k == 2) &&
         cap >= 0 && e_per_rank >= 1);
   if (S == 0) return MOE_OK;
@@ -358,6 +358,8 @@ int moe_dispatch_p2p(const void* x, int64_t S, int64_t row_bytes, int E, int k, 
   a.peer_token = peer_token, a.peer_prob = peer_prob, a.e_per_rank = e_per_rank;
   a.out_dropped = static_cast<uint8_t*>(out_dropped);
   a.row_index = row_index;
+  a.peer_src = peer_src;
+  a.my_rank = my_rank;
   return moe::launch_scatter(a, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -395,6 +397,25 @@ int moe_grouped_gemm_bf16_combine_rows(const void* A, int64_t a_rows, int K, con
                                        row_start, 0, rows, 0, weight_idx, max_group_rows, 2,
                                        reinterpret_cast<cudaStream_t>(stream), row_token, row_prob,
                                        x_rows, out_rows, 1);
+}
+
+int moe_grouped_gemm_bf16_push(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
+                               int N, const float* bias, int num_groups, const int32_t* row_start,
+                               const int32_t* rows, const int32_t* weight_idx,
+                               int64_t max_group_rows, int combine, const int32_t* row_token,
+                               const float* row_prob, const int32_t* row_src,
+                               void* const* push_base, const void* x_rows, void* stream) {
+  CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1);
+  CHECK(max_group_rows >= 0 && (combine == 0 || combine == 1));
+  if (a_rows == 0 || max_group_rows == 0) return MOE_OK;
+  CHECK(A && B && row_start && rows && row_token && row_src && push_base);
+  if (combine) CHECK(row_prob && x_rows);
+  // combine = 1: act 2 (EPI_BIAS_COMBINE, x = the receive row itself); 0: bias only
+  return moe::launch_grouped_gemm_bf16(A, a_rows, K, B, b_rows, N, bias, nullptr, num_groups,
+                                       row_start, 0, rows, 0, weight_idx, max_group_rows,
+                                       combine ? 2 : 0, reinterpret_cast<cudaStream_t>(stream),
+                                       row_token, row_prob, x_rows, nullptr, combine ? 1 : 0, 0,
+                                       nullptr, push_base, row_src);
 }
 
 }  // extern "C"

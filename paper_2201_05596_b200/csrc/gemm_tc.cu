@@ -113,6 +113,11 @@ struct GemmArgs {
   int64_t c_cap;
   int64_t c_tokens;           // S
   int* c_done;                // zeroed: expert-tile epilogue warps done storing y
+  const int32_t* c_row_index; // [S, k] row of y per choice (-1 dropped), or null: e*cap+slot
+  // EP push return (EPI_BIAS / EPI_BIAS_COMBINE): valid row r is stored to rank
+  // row_src[r]'s buffer push_base[row_src[r]] at row row_token[r] (over NVLink)
+  void* const* push_base;
+  const int32_t* row_src;
   int tma_store;    // EPI_BIAS / EPI_BIAS_GELU: whole-box TMA stores through map_d
   int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
   int raster;       // tile order (see tile_at)
@@ -757,6 +762,10 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           named_bar_sync(2, EW * 32);
         }
         __nv_bfloat16* drow = args.D + out_row * N;
+        const bool push = args.push_base != nullptr && valid;
+        if (push && EPI == EPI_BIAS)
+          drow = static_cast<__nv_bfloat16*>(args.push_base[args.row_src[out_row]]) +
+                 (int64_t)args.row_token[out_row] * N;
         const __nv_bfloat16* xrow = nullptr;
         float prob = 0.f;
         __nv_bfloat16* arow = nullptr;  // EPI_GELU_SAVE: pre-activation output row
@@ -765,6 +774,8 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           prob = valid ? args.row_prob[out_row] : 0.f;
           drow = args.out + (args.x_by_row ? out_row : tok) * N;
           xrow = args.x_resid + (args.x_by_row ? out_row : tok) * N;
+          if (push)  // the combined row goes straight to its source's output (NVLink)
+            drow = static_cast<__nv_bfloat16*>(args.push_base[args.row_src[out_row]]) + tok * N;
         }
         if constexpr (EPI == EPI_GELU_BWD) xrow = args.x_resid + out_row * N;
         if constexpr (EPI == EPI_GELU_SAVE) arow = args.out + out_row * N;
@@ -788,10 +799,16 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             if (valid) {
               int e0 = 0;
               for (int j = 0; j < args.c_k; ++j) {
-                const int sl = args.c_slots[c_t * args.c_k + j];
-                if (sl < 0) continue;
+                int64_t r;
+                if (args.c_row_index != nullptr) {
+                  r = args.c_row_index[c_t * args.c_k + j];
+                  if (r < 0) continue;
+                } else {
+                  const int sl = args.c_slots[c_t * args.c_k + j];
+                  if (sl < 0) continue;
+                  r = (int64_t)args.c_ids[c_t * args.c_k + j] * args.c_cap + sl;
+                }
                 const int e = args.c_ids[c_t * args.c_k + j];
-                const int64_t r = (int64_t)e * args.c_cap + sl;
                 const float pj = args.c_gp[c_t * args.c_k + j];
                 if (cn == 0) { cr0 = r; cp0 = pj; e0 = e; }
                 else if (e < e0) { cr1 = cr0; cp1 = cp0; cr0 = r; cp0 = pj; }
@@ -1056,7 +1073,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
               pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
               pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-              if (args.stream_hint)
+              if (args.stream_hint && !push)
                 st_global_hint(dst + q, pk, pol_stream);
               else
                 dst[q] = pk;
@@ -1262,6 +1279,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       if (lane == 0) bulk_wait_group_all();
       __syncwarp();
     }
+    // pushed rows (NVLink stores to the sources) performed before the kernel ends
+    // and the caller's flag barrier releases them
+    if (args.push_base != nullptr) __threadfence_system();
     if constexpr (EPI == EPI_GATE) {
       if (args.probsum != nullptr) {  // one global atomic per expert per CTA
         named_bar_sync(1, 128);
@@ -1572,7 +1592,8 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              const int32_t* weight_idx, int64_t max_group_rows, int act,
                              cudaStream_t st, const int32_t* row_token, const float* row_prob,
                              const void* x_resid, void* out, int x_by_row, int pad_scratch,
-                             const int32_t* a_gather) {
+                             const int32_t* a_gather, void* const* push_base,
+                             const int32_t* row_src) {
   if (G < 1 || G > kMaxGroups || K < 1 || N < 1 || (K % 8) != 0) return MOE_EINVAL;
   int BN = 256;
   if (N <= 32) BN = 32;
@@ -1618,6 +1639,8 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.out = (__nv_bfloat16*)out;
   a.x_by_row = x_by_row;
   a.a_gather = a_gather;
+  a.push_base = push_base;
+  a.row_src = row_src;
   a.tile_counter = dyn_counter(st, K, N);
   a.stream_hint = stream_hint;
   a.raster = raster;
@@ -1795,7 +1818,8 @@ int launch_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int
                               const int32_t* rows, const int32_t* weight_idx,
                               int64_t max_group_rows, int mode, int rc_group, const int32_t* ids,
                               const int32_t* slots, const float* gp, int k, int64_t cap,
-                              const void* x, void* out, int64_t S, cudaStream_t st) {
+                              const void* x, void* out, int64_t S, cudaStream_t st,
+                              const int32_t* row_index) {
   if (G < 1 || G > kMaxGroups || K < 8 || (K % 8) || N < 8 || (N % 8) || row_stride < 1)
     return MOE_EINVAL;
   static const int stream_hint = [] {
@@ -1847,9 +1871,11 @@ int launch_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int
       default: return launch_tc<256, 4, EPI_BIAS_GELU, 1, 4>(ma, mb, a, max_tiles, st, nullptr, 0, &ma2);
     }
   }
-  if (mode != 0 || rc_group < 0 || rc_group > G || ids == nullptr || slots == nullptr ||
-      gp == nullptr || x == nullptr || out == nullptr || k < 1 || k > 2)
+  if (mode != 0 || rc_group < 0 || rc_group > G || ids == nullptr ||
+      (slots == nullptr && row_index == nullptr) || gp == nullptr || x == nullptr ||
+      out == nullptr || k < 1 || k > 2)
     return MOE_EINVAL;
+  a.c_row_index = row_index;
   a.has_rc = 1;
   a.rc_group = rc_group;
   a.c_ids = ids;

@@ -44,6 +44,12 @@ struct ScatterArgs {
   int32_t* const* peer_token = nullptr;
   float* const* peer_prob = nullptr;
   int e_per_rank = 1;
+  // EP push return: the owner's GEMM2 epilogue stores each row straight back to its
+  // source. Per receive row the owner gets the source rank (peer_src) and the
+  // return row t*k + j (peer_token); row_index (S, k) becomes that return row
+  // (or -1 when dropped)
+  int32_t* const* peer_src = nullptr;
+  int my_rank = 0;
 };
 
 int launch_scatter(const ScatterArgs& args, cudaStream_t st);
@@ -60,7 +66,8 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              cudaStream_t st, const int32_t* row_token = nullptr,
                              const float* row_prob = nullptr, const void* x_resid = nullptr,
                              void* out = nullptr, int x_by_row = 0, int pad_scratch = 0,
-                             const int32_t* a_gather = nullptr);
+                             const int32_t* a_gather = nullptr, void* const* push_base = nullptr,
+                             const int32_t* row_src = nullptr);
 
 int launch_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int64_t a2_rows,
                               int a2_group, int K, const void* B, int64_t b_rows, int N,
@@ -68,7 +75,8 @@ int launch_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int
                               const int32_t* rows, const int32_t* weight_idx,
                               int64_t max_group_rows, int mode, int rc_group, const int32_t* ids,
                               const int32_t* slots, const float* gp, int k, int64_t cap,
-                              const void* x, void* out, int64_t S, cudaStream_t st);
+                              const void* x, void* out, int64_t S, cudaStream_t st,
+                              const int32_t* row_index = nullptr);
 
 int launch_wgrad_bf16(const void* X, int64_t x_rows, int P, const void* Y, int Q, int G,
                       int64_t k_stride, const int32_t* k_rows, int64_t k_rows_const, void* D,

@@ -330,22 +330,27 @@ __global__ void scatter_kernel(ScatterArgs a) {
         uint8_t* base = a.buf;
         int32_t* rtok = a.row_token;
         float* rprob = a.row_prob;
+        int32_t* rsrc = nullptr;
         if (a.peer_buf != nullptr) {  // EP over NVLink: the owner rank's receive buffer
           const int owner = e / a.e_per_rank;
           base = a.peer_buf[owner];
           rtok = a.peer_token[owner];
           rprob = a.peer_prob[owner];
+          if (a.peer_src != nullptr) rsrc = a.peer_src[owner];
         }
         if (j == 0) { dst0 = d; base0 = base; } else { dst1 = d; base1 = base; }
         if (lane == 0) {
           if (a.occupied != nullptr) a.occupied[d] = 1;
           if (rtok != nullptr) {
-            rtok[d] = (int32_t)t;
+            // push return: where the owner sends the row back (source rank, row t*k+j)
+            rtok[d] = rsrc != nullptr ? (int32_t)(t * k + j) : (int32_t)t;
             rprob[d] = a.gate_probs[t * k + j];
+            if (rsrc != nullptr) rsrc[d] = a.my_rank;
           }
         }
       }
-      if (a.row_index != nullptr && lane == 0) a.row_index[t * k + j] = (int32_t)d;
+      if (a.row_index != nullptr && lane == 0)
+        a.row_index[t * k + j] = (a.peer_src != nullptr && d >= 0) ? (int32_t)(t * k + j) : (int32_t)d;
     }
     V* d0 = nullptr;
     V* d1 = nullptr;

@@ -170,16 +170,15 @@ class EPMoeLayer:
             self.b1[i] = _t(p.b1, dev, torch.float32).reshape(F)
             self.b2[i] = _t(p.b2, dev, torch.float32).reshape(M)
         self.shared = DenseFfn(shared, M, dtype, dev) if spec.residual else None
-        # "p2p": dispatch stores rows into the owners' receive buffers and the GEMM2
-        # epilogue stores combined rows into the sources' outputs, over NVLink peer
-        # memory (k=1, no shared MLP); "nccl": two all_to_all_single exchanges.
-        p2p_ok = self.k == 1 and self.shared is None
+        # "p2p": dispatch stores rows into the owners' receive buffers and the owners'
+        # GEMM2 epilogue stores every row straight back into its source (combined
+        # into the output for k=1 layers; expert outputs into a return buffer that
+        # the source combines locally for k=2 / Residual-MoE), over NVLink peer
+        # memory; "nccl": two all_to_all_single exchanges.
         if transport == "auto":
-            transport = "p2p" if (p2p_ok and schedule == "flat") else "nccl"
+            transport = "p2p" if schedule == "flat" else "nccl"
         if schedule != "flat" and transport != "nccl":
             raise ValueError(f"schedule {schedule!r} runs on the nccl transport")
-        if transport == "p2p" and not p2p_ok:
-            raise ValueError("the peer-memory transport covers k=1 layers without a shared MLP")
         if transport not in ("p2p", "nccl"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
@@ -189,6 +188,8 @@ class EPMoeLayer:
         # GEMMs leave free, from a second stream)
         if chunks < 1 or (chunks > 1 and transport != "p2p"):
             raise ValueError("chunks > 1 needs the p2p transport")
+        if chunks > 1 and (self.k != 1 or self.shared is not None):
+            raise ValueError("the chunked p2p pipeline covers k=1 layers without a shared MLP")
         self.chunks, self.comm_sms = int(chunks), int(comm_sms)
         self.exchanger = Exchanger(group, schedule, gpus_per_node) if transport == "nccl" else None
         self._ws: dict = {}
@@ -256,8 +257,9 @@ class EPMoeLayer:
             ret=torch.empty((max(S * k, 1), M), dtype=self.dtype, device=dev),
         )
         if self.shared is not None:
-            ws["hs"] = torch.empty((S, F), dtype=self.dtype, device=dev)
-            ws["ys"] = torch.empty((S, M), dtype=self.dtype, device=dev)
+            ws["hs"] = torch.empty((max(S, 1), F), dtype=self.dtype, device=dev)
+            ws["sh_rows"] = torch.tensor([S], **i32)
+            ws["sh_w"] = torch.zeros(1, **i32)
         self._ws[S] = ws
         return ws
 
@@ -352,16 +354,26 @@ class EPMoeLayer:
                       max_rows, _lib.MOE_ACT_NONE, st)
         ph("all_to_all_return")
         self.exchanger.all_to_all(ws["ret"], ws["y"], C.T)
-        shared_out = None
-        if self.shared is not None:
+        if self.shared is not None and S:
+            # shared MLP GEMM1, then GEMM2 with the combine + residual adds in its
+            # epilogue, reading the returned rows (the single-GPU arithmetic)
             ph("shared_mlp")
-            shared_out = self.shared(x, ws["hs"], ws["ys"])
+            sh = self.shared
+            _lib.call("moe_grouped_gemm_bf16", x.data_ptr(), S, M, sh.w1.data_ptr(), F, F,
+                      sh.b1.data_ptr(), ws["hs"].data_ptr(), 1, None, 0, None, S, None, S,
+                      _lib.MOE_ACT_GELU | _lib.MOE_GEMM_PAD_SCRATCH, st)
+            _lib.call("moe_residual_gemm_bf16", ws["hs"].data_ptr(), S, None, 0, 0, F,
+                      sh.w2.data_ptr(), M, M, sh.b2.data_ptr(), ws["ret"].data_ptr(), 1, S,
+                      ws["sh_rows"].data_ptr(), ws["sh_w"].data_ptr(), S, 0, 0, ids.data_ptr(),
+                      None, gp.data_ptr(), k, cap, x.data_ptr(), out.data_ptr(), S,
+                      ws["row_index"].data_ptr(), st)
+            ph(None)
+            return out
         ph("combine")
         if S:
             _lib.call("moe_combine", ws["ret"].data_ptr(), _lib.MOE_BF16, S, M, E, k, cap,
                       ids.data_ptr(), ws["slots"].data_ptr(), ws["row_index"].data_ptr(),
-                      gp.data_ptr(), _lib.MOE_F32, x.data_ptr(), _lib.ptr(shared_out),
-                      out.data_ptr(), 1, st)
+                      gp.data_ptr(), _lib.MOE_F32, x.data_ptr(), None, out.data_ptr(), 1, st)
         ph(None)
         return out
 
@@ -408,14 +420,20 @@ class EPMoeLayer:
             return (n + 255) // 256 * 256
 
         C = self.chunks
+        # push return: k=1 layers without a shared MLP get two alternating output
+        # slots the owners store combined rows into; others an (S*k)-row return buffer
+        push1 = k == 1 and self.shared is None
         off_recv = 0
         off_tok = off_recv + al(rmax * M * 2)
         off_prob = off_tok + al(rmax * 4)
-        off_ret = off_prob + al(rmax * 4)
-        off_cnt = off_ret + al(rmax * M * 2)
+        off_src = off_prob + al(rmax * 4)
+        off_ret = off_src + al(rmax * 4)  # owner-local combined rows (chunked pull path)
+        off_cnt = off_ret + (al(rmax * M * 2) if C > 1 else 0)
         off_sig = off_cnt + al(self.world * C * self.E * 4)
         off_sig2 = off_sig + al(64 * 4)  # second barrier channel (the comm stream)
-        total = off_sig2 + al(64 * 4)
+        off_back = off_sig2 + al(64 * 4)  # output slots (push1) / return buffer
+        back_rows = 2 * S if push1 else S * k
+        total = off_back + al(max(back_rows, 1) * M * 2)
         region = IpcRegion(total, self.group, self.dev)
         i32 = dict(dtype=torch.int32, device=self.dev)
         G = self.E_loc
@@ -424,13 +442,22 @@ class EPMoeLayer:
             recv=region.tensor(off_recv, (rmax, M), torch.bfloat16),
             row_token=region.tensor(off_tok, (rmax,), torch.int32),
             row_prob=region.tensor(off_prob, (rmax,), torch.float32),
-            ret=region.tensor(off_ret, (rmax, M), torch.bfloat16),
+            ret=region.tensor(off_ret, (rmax, M), torch.bfloat16) if C > 1 else None,
+            row_src=region.tensor(off_src, (rmax,), torch.int32), peer_src=region.ptr_table(off_src),
+            push1=push1,
+            oslot=[region.tensor(off_back + i * S * M * 2, (S, M), torch.bfloat16)
+                   for i in range(2)] if push1 else None,
+            peer_oslot=[region.ptr_table(off_back + i * S * M * 2) for i in range(2)]
+            if push1 else None,
+            retbuf=None if push1 else region.tensor(off_back, (max(S * k, 1), M), torch.bfloat16),
+            peer_retbuf=None if push1 else region.ptr_table(off_back), flip=0,
             signal=region.tensor(off_sig, (64,), torch.int32),
             signal2=region.tensor(off_sig2, (64,), torch.int32),
             counts=region.tensor(off_cnt, (self.world * C * self.E,), torch.int32),
             peer_cnt=region.ptr_table(off_cnt),
             peer_recv=region.ptr_table(off_recv), peer_tok=region.ptr_table(off_tok),
-            peer_prob=region.ptr_table(off_prob), peer_ret=region.ptr_table(off_ret),
+            peer_prob=region.ptr_table(off_prob),
+            peer_ret=region.ptr_table(off_ret) if C > 1 else None,
             peer_sig=region.ptr_table(off_sig), peer_sig2=region.ptr_table(off_sig2),
             slot_base=torch.empty(C * self.E, **i32), row_base=torch.empty(C * self.E, **i32),
             seg_start=torch.empty(C * G, **i32), seg_rows=torch.empty(C * G, **i32),
@@ -439,6 +466,9 @@ class EPMoeLayer:
             h=torch.empty((rmax, self.F), dtype=self.dtype, device=self.dev),
             err=torch.zeros(1, **i32),
         )
+        if self.shared is not None:  # the source's shared MLP: one group of S token rows
+            st.update(hs=torch.empty((max(S, 1), self.F), dtype=self.dtype, device=self.dev),
+                      sh_rows=torch.tensor([S], **i32), sh_w=torch.zeros(1, **i32))
         dist.barrier(group=self.group)
         self._p2p[S] = st
         return st
@@ -458,6 +488,13 @@ class EPMoeLayer:
                 raise RuntimeError("expert-parallel peer barrier timed out")
 
     def _forward_p2p(self, x: torch.Tensor, out: torch.Tensor | None, timer):
+        """Peer-memory forward: gate -> counts all-gather over peer memory -> device
+        plan -> dispatch straight into the owners' receive buffers -> barrier ->
+        owner GEMM1 / GEMM2 whose epilogue stores every row back to its source over
+        NVLink -> barrier -> (k=2 / Residual-MoE) local combine. k=1 layers without
+        a shared MLP are combined by the owner's epilogue into the source's output
+        slot (alternating between two per batch size; returned when ``out`` is None,
+        copied into ``out`` otherwise)."""
         if self.chunks > 1:
             return self._forward_p2p_chunked(x, out, timer)
         if x.device != self.dev:
@@ -472,7 +509,14 @@ class EPMoeLayer:
         stream = _lib.stream_ptr()
         ph = _Phases(timer)
         ids, gp, lr, tc = ws["ids"], ws["gp"], ws["local_rank"], ws["tile_counts"]
-        out = torch.empty_like(x) if out is None else out
+        push1 = st["push1"]
+        if push1:
+            j = st["flip"]
+            st["flip"] ^= 1
+            slot, dest = st["oslot"][j], st["peer_oslot"][j]
+        else:
+            slot, dest = None, st["peer_retbuf"]
+            out = torch.empty_like(x) if out is None else out
         ph("gate")
         if S:
             _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k, None,
@@ -501,7 +545,8 @@ class EPMoeLayer:
                       st["slot_base"].data_ptr(), st["row_base"].data_ptr(), self.E_loc,
                       st["peer_recv"].data_ptr(), st["peer_tok"].data_ptr(),
                       st["peer_prob"].data_ptr(), ws["slots"].data_ptr(),
-                      ws["row_index"].data_ptr(), out.data_ptr(), stream)
+                      ws["row_index"].data_ptr(), _lib.ptr(slot), st["peer_src"].data_ptr(),
+                      self.rank, stream)
         self._barrier(st)
         G = self.E_loc
         if cap:
@@ -511,19 +556,46 @@ class EPMoeLayer:
                       st["h"].data_ptr(), G, st["seg_start"].data_ptr(), 0,
                       st["seg_rows"].data_ptr(), 0, st["seg_w"].data_ptr(), cap,
                       _lib.MOE_ACT_GELU, stream)
-            ph("gemm2")  # + combine + residual, stored in the receive layout
-            _lib.call("moe_grouped_gemm_bf16_combine_rows", st["h"].data_ptr(), st["rmax"], F,
+            # GEMM2 + bias (+ combine and residual for k=1), every row stored straight
+            # back to its source rank over NVLink
+            ph("gemm2_push")
+            _lib.call("moe_grouped_gemm_bf16_push", st["h"].data_ptr(), st["rmax"], F,
                       self.w2.data_ptr(), self.E_loc * M, M, self.b2.data_ptr(), G,
                       st["seg_start"].data_ptr(), st["seg_rows"].data_ptr(),
-                      st["seg_w"].data_ptr(), cap, st["row_token"].data_ptr(),
-                      st["row_prob"].data_ptr(), st["recv"].data_ptr(), st["ret"].data_ptr(),
-                      stream)
+                      st["seg_w"].data_ptr(), cap, 1 if push1 else 0, st["row_token"].data_ptr(),
+                      st["row_prob"].data_ptr(), st["row_src"].data_ptr(), dest.data_ptr(),
+                      st["recv"].data_ptr(), stream)
+        if self.shared is not None and S:
+            ph("shared_mlp1")  # the source's shared MLP, first half (replicated weights)
+            sh = self.shared
+            _lib.call("moe_grouped_gemm_bf16", x.data_ptr(), S, M, sh.w1.data_ptr(), F, F,
+                      sh.b1.data_ptr(), st["hs"].data_ptr(), 1, None, 0, None, S, None, S,
+                      _lib.MOE_ACT_GELU | _lib.MOE_GEMM_PAD_SCRATCH, stream)
+        ph("return_barrier")
         self._barrier(st)
-        ph("pull_p2p")
+        if push1:
+            ph(None)
+            if out is None:
+                return slot
+            out.copy_(slot)
+            return out
         if S:
-            _lib.call("moe_pull_rows_p2p", S, M * 2, E, k, ids.data_ptr(),
-                      ws["row_index"].data_ptr(), self.E_loc, st["peer_ret"].data_ptr(),
-                      out.data_ptr(), stream)
+            if self.shared is not None:
+                # out = (x + sum_j p_j y_j) + shared MLP(x): the shared GEMM2 epilogue
+                # reads the returned expert rows (arch.py:389-391)
+                ph("shared_mlp2_combine")
+                sh = self.shared
+                _lib.call("moe_residual_gemm_bf16", st["hs"].data_ptr(), S, None, 0, 0, F,
+                          sh.w2.data_ptr(), M, M, sh.b2.data_ptr(), st["retbuf"].data_ptr(), 1,
+                          S, st["sh_rows"].data_ptr(), st["sh_w"].data_ptr(), S, 0, 0,
+                          ids.data_ptr(), None, gp.data_ptr(), k, cap, x.data_ptr(),
+                          out.data_ptr(), S, ws["row_index"].data_ptr(), stream)
+            else:
+                ph("combine")
+                _lib.call("moe_combine", st["retbuf"].data_ptr(), _lib.MOE_BF16, S, M, E, k, cap,
+                          ids.data_ptr(), ws["slots"].data_ptr(), ws["row_index"].data_ptr(),
+                          gp.data_ptr(), _lib.MOE_F32, x.data_ptr(), None, out.data_ptr(), 1,
+                          stream)
         ph(None)
         return out
 
@@ -587,7 +659,7 @@ class EPMoeLayer:
                       st["row_base"][c * E:].data_ptr(), G, st["peer_recv"].data_ptr(),
                       st["peer_tok"].data_ptr(), st["peer_prob"].data_ptr(),
                       slots[c * Sc:].data_ptr(), rix[c * Sc:].data_ptr(),
-                      out[c * Sc:].data_ptr(), _lib.stream_ptr())
+                      out[c * Sc:].data_ptr(), None, 0, _lib.stream_ptr())
             _lib.call("moe_set_launch_limits", 0, 0)
             self._barrier(st, channel=1)
 

@@ -129,19 +129,24 @@ def forward_train(layer, x: torch.Tensor) -> torch.Tensor:
                   _lib.MOE_ACT_GELU_SAVE, a)
             _gemm(h, E * cap, F, layer.w2, M, layer.b2, y, E, cap, load, 0, cap, _lib.MOE_GEMM_PAD_SCRATCH)
     sh_ctx = None
-    shared_out = None
     if layer.shared is not None and S:
+        # shared MLP: GEMM1 saving its pre-activation, then GEMM2 with the combine and
+        # both residual adds in its epilogue (the inference arithmetic, arch.py:389-391)
         s = layer.shared
+        i32 = dict(dtype=torch.int32, device=dev)
         a_s = torch.empty((S, F), dtype=torch.bfloat16, device=dev)
         h_s = torch.empty_like(a_s)
-        shared_out = torch.empty_like(x)
         _gemm(x, S, M, s.w1, F, s.b1, h_s, 1, 0, None, S, S, _lib.MOE_ACT_GELU_SAVE, a_s)
-        _gemm(h_s, S, F, s.w2, M, s.b2, shared_out, 1, 0, None, S, S, _lib.MOE_GEMM_PAD_SCRATCH)
+        sh_rows, sh_w = torch.tensor([S], **i32), torch.zeros(1, **i32)  # (kept alive)
+        _lib.call("moe_residual_gemm_bf16", h_s.data_ptr(), S, None, 0, 0, F, s.w2.data_ptr(), M,
+                  M, s.b2.data_ptr(), y.data_ptr(), 1, S, sh_rows.data_ptr(), sh_w.data_ptr(), S,
+                  0, 0, ids.data_ptr(), slots.data_ptr(), gp.data_ptr(), k, cap, x.data_ptr(),
+                  out.data_ptr(), S, None, st)
         sh_ctx = (a_s, h_s)
-    if S and not fused:
+    elif S and not fused:
         _lib.call("moe_combine", y.data_ptr(), _lib.MOE_BF16, S, M, E, k, cap, ids.data_ptr(),
                   slots.data_ptr(), None, gp.data_ptr(), _lib.MOE_F32, x.data_ptr(),
-                  _lib.ptr(shared_out), out.data_ptr(), 1, st)
+                  None, out.data_ptr(), 1, st)
     layer._train_ctx = dict(x=x, S=S, cap=cap, logits=logits, ids=ids.clone(), gp=gp.clone(),
                             slots=slots, load=load, xbuf=xbuf, a=a, h=h, y=y, shared=sh_ctx)
     return out

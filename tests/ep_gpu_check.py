@@ -147,8 +147,6 @@ def main():
     ]
     for c in cases:
         for transport in ("nccl", "p2p"):
-            if transport == "p2p" and (c[3] != 1 or c[5]):
-                continue
             dropped = run_case(*c, transport=transport)
             if dist.get_rank() == 0:
                 print(f"ep ok same_device={int(SAME_DEVICE)} world={world} transport={transport} case={c} "
@@ -164,8 +162,6 @@ def main():
         residual = bool(rng.random() < 0.3)
         c = (S_loc, M, E, k, cf, residual, float(rng.uniform(0, 1.5)), 100 + i)
         for transport in ("nccl", "p2p"):
-            if transport == "p2p" and (k != 1 or residual):
-                continue
             run_case(*c, transport=transport)
             if dist.get_rank() == 0:
                 print(f"ep ok same_device={int(SAME_DEVICE)} world={world} random-case via {transport} case={c}", flush=True)

@@ -38,7 +38,7 @@ def _run(n: int, port: int, same_device: bool, timeout: int = 1500) -> str:
 
 def _check_counts(out: str, n: int) -> None:
     assert out.count("transport=nccl") == 5
-    assert out.count("transport=p2p ") == 2
+    assert out.count("transport=p2p ") == 5  # every case: k=2 and Residual-MoE included
     assert out.count("transport=p2p-chunked") == 4
     if n % 2 == 0:
         assert out.count("schedule=hierarchical") == 3
