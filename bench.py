@@ -608,7 +608,7 @@ def run_gpu(args):
     hbm, tf_burst, tf_sus, src = peaks()
 
     def gemm_ms_of(ph: dict) -> float:
-        return sum(v for kk, v in ph.items() if kk.startswith("gemm") or kk == "shared_mlp")
+        return sum(v for kk, v in ph.items() if kk.startswith("gemm") or kk.startswith("shared_mlp"))
 
     # ---- sustained: the same step looped for >= 2 s (the timed region above is a
     # short burst at full clock; this is the 1 kW power-capped steady state)
