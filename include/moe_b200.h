@@ -302,6 +302,11 @@ int moe_bwd_dx_bf16(const void* dout, const void* dxr, int64_t S, int M, int E, 
 
 /* Device memory shareable with the other ranks' processes (cudaMalloc +
  * cudaIpc handles; 64-byte handles, exchanged by the caller). Zero-filled. */
+/* Direct peer access from the current device to peer_device's memory (one
+ * process driving several GPUs, e.g. tools/nvlink_ep_probe.py); 0 if enabled
+ * or already enabled. */
+int moe_enable_peer_access(int peer_device);
+
 int moe_ipc_malloc(size_t bytes, void** ptr);
 int moe_ipc_free(void* ptr);
 int moe_ipc_get_handle(void* ptr, void* handle64);

@@ -55,6 +55,7 @@ SIGNATURES = {
                                    _I, _P]),
     "moe_grouped_gemm_bf16_combine": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _L, _P, _L, _P,
                                            _L, _P, _P, _P, _P, _P, _P]),
+    "moe_enable_peer_access": (_I, [_I]),
     "moe_ipc_malloc": (_I, [_Z, _P]),
     "moe_ipc_free": (_I, [_P]),
     "moe_ipc_get_handle": (_I, [_P, _P]),
@@ -165,6 +166,7 @@ def dtype_code(dt: torch.dtype) -> int:
 # ---------------------------------------------------------------------------
 
 _NON_LAUNCH = {"moe_abi_version", "moe_plan_workspace_bytes", "moe_scan_workspace_bytes",
+               "moe_enable_peer_access",
                "moe_load_balance_workspace_bytes",
                "moe_ipc_malloc", "moe_ipc_free", "moe_ipc_get_handle", "moe_ipc_open_handle",
                "moe_ipc_close_handle"}

@@ -276,6 +276,16 @@ int moe_ipc_malloc(size_t bytes, void** ptr) {
 
 int moe_ipc_free(void* ptr) { return ptr ? (int)cudaFree(ptr) : MOE_OK; }
 
+int moe_enable_peer_access(int peer_device) {
+  CHECK(peer_device >= 0);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return MOE_OK;
+  }
+  return (int)e;
+}
+
 int moe_ipc_get_handle(void* ptr, void* handle64) {
   CHECK(ptr && handle64);
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");

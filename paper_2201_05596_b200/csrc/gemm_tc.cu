@@ -45,7 +45,15 @@ namespace moe {
 //     every expert tile has stored (device counter) and emits
 //     out[t] = (x[t] + sum_j p_j y[e_j*cap + slot_j]) + (acc + b2_shared).
 enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2, EPI_BIAS_COMBINE = 3, EPI_GELU_SAVE = 4,
-       EPI_GELU_BWD = 5, EPI_WGRAD = 6, EPI_WGRAD_ACC = 7, EPI_BIAS_RESID = 8 };
+       EPI_GELU_BWD = 5, EPI_WGRAD = 6, EPI_WGRAD_ACC = 7, EPI_BIAS_RESID = 8,
+       EPI_COMBINE_PUSH = 9 };
+// EPI_COMBINE_PUSH: EPI_BIAS_COMBINE for the EP push return (rows stored to the
+// sources over NVLink through the coalescing smem stage); its own instance so the
+// single-GPU fused-combine GEMM keeps its registers
+template <int EPI>
+constexpr bool is_combine() {
+  return EPI == EPI_BIAS_COMBINE || EPI == EPI_COMBINE_PUSH;
+}
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
@@ -175,9 +183,12 @@ constexpr int out_bufs() {
 }
 template <int EPI, int EW, int CG, int BN = 256>
 constexpr int out_stage_bytes() {
+  // (the 2-CTA fused-combine GEMM stages one 32 x 32 chunk per warp for the
+  // coalesced row stores of the EP push return)
   return (EPI == EPI_WGRAD ||
           (CG == 2 && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID)))
-             ? EW * out_bufs<BN>() * 2048 : 0;
+             ? EW * out_bufs<BN>() * 2048
+             : ((CG == 2 && EPI == EPI_COMBINE_PUSH && BN <= 256) ? EW * 2048 : 0);
 }
 
 // CL = cluster size: CG (one CTA pair per cluster) or 2*CG = 4: two pairs run the
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   // BN = 512 forward tiles hand the accumulator over in kParts column parts of
   // kPW (tfull/tempty[j]; N = kPW MMAs) so the epilogue overlaps the MMAs
   // without a second accumulator buffer
-  constexpr bool kSplit = kNI == 2 && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_COMBINE);
+  constexpr bool kSplit = kNI == 2 && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || is_combine<EPI>());
   // (two N=256 halves: N=128 parts re-read A from smem twice as often and measured slower)
   constexpr int kParts = kSplit ? 2 : 1;
   constexpr int kPW = BN / kParts;
@@ -762,14 +773,16 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           named_bar_sync(2, EW * 32);
         }
         __nv_bfloat16* drow = args.D + out_row * N;
-        const bool push = args.push_base != nullptr && valid;
+        // (push launches use <= 256-column tiles: no push code in the 512-column ones)
+        const bool push = BN <= 256 && (EPI == EPI_BIAS || EPI == EPI_COMBINE_PUSH) &&
+                          args.push_base != nullptr && valid;
         if (push && EPI == EPI_BIAS)
           drow = static_cast<__nv_bfloat16*>(args.push_base[args.row_src[out_row]]) +
                  (int64_t)args.row_token[out_row] * N;
         const __nv_bfloat16* xrow = nullptr;
         float prob = 0.f;
         __nv_bfloat16* arow = nullptr;  // EPI_GELU_SAVE: pre-activation output row
-        if constexpr (EPI == EPI_BIAS_COMBINE) {
+        if constexpr (is_combine<EPI>()) {
           const int64_t tok = valid ? args.row_token[out_row] : 0;
           prob = valid ? args.row_prob[out_row] : 0.f;
           drow = args.out + (args.x_by_row ? out_row : tok) * N;
@@ -820,7 +833,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             xrow = args.x_resid + c_t * N;
           }
         }
-        constexpr bool kLoadX = EPI == EPI_BIAS_COMBINE || EPI == EPI_GELU_BWD;
+        constexpr bool kLoadX = is_combine<EPI>() || EPI == EPI_GELU_BWD;
         // residual row chunks (COMBINE) are prefetched one chunk ahead
         auto load_x = [&](int c, uint4 (&xq)[4]) {
           const int col0 = nb * BN + chunk_col(c);
@@ -900,9 +913,16 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             }
             continue;
           }
-          constexpr bool kTmaEpi = out_stage_bytes<EPI, EW, CG, BN>() > 0 && EPI != EPI_WGRAD;
+          constexpr bool kTmaEpi = out_stage_bytes<EPI, EW, CG, BN>() > 0 && EPI != EPI_WGRAD &&
+                                   !is_combine<EPI>();
+          // EP push return: rows go to scattered peer rows, so the warp stages its
+          // 32 x 32 chunk in smem and stores it 4 lanes per row (full 64-B row
+          // segments per NVLink write instead of 16-B pieces of 32 different rows)
+          constexpr bool kCoalOK = out_stage_bytes<EPI, EW, CG, BN>() > 0 && BN <= 256 &&
+                                   (EPI == EPI_BIAS || EPI == EPI_COMBINE_PUSH);
+          const bool coal = kCoalOK && args.push_base != nullptr && vec_ok && col0 + 32 <= N;
           if (col0 >= N) continue;
-          if (!valid && !(kTmaEpi && args.tma_store)) continue;
+          if (!valid && !(kTmaEpi && args.tma_store) && !coal) continue;
           float v[32];
           const float4* b4 = reinterpret_cast<const float4*>(sbias + cl);
 #pragma unroll
@@ -1025,7 +1045,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
                          gelu_tanh_grad_fast(__bfloat162float(xrow[col0 + i]));
             }
           }
-          if constexpr (EPI == EPI_BIAS_COMBINE) {
+          if constexpr (is_combine<EPI>()) {
             if (args.D != nullptr) {  // training: also keep y = acc + b2 (row layout) for backward
               __nv_bfloat16* yrow = args.D + out_row * N;
               if (vec_ok && col0 + 32 <= N) {
@@ -1061,6 +1081,34 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) pk32[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
               stage_store(pk32);
+              continue;
+            }
+          }
+          if constexpr (kCoalOK) {
+            if (coal) {  // warp-uniform: every lane of the warp is here (invalid rows masked)
+              uint8_t* ob = smem + L::kOutOff + (warp - 2) * (out_stage_bytes<EPI, EW, CG, BN>() / EW);
+              __syncwarp();
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int chunk = q ^ ((lane >> 1) & 3);
+                *reinterpret_cast<uint4*>(ob + lane * 64 + chunk * 16) =
+                    make_uint4(pack_bf16x2(v[8 * q + 0], v[8 * q + 1]),
+                               pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                               pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
+                               pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+              }
+              __syncwarp();
+              const unsigned long long mine =
+                  valid ? reinterpret_cast<unsigned long long>(drow + col0) : 0ull;
+#pragma unroll
+              for (int it = 0; it < 4; ++it) {
+                const int r = it * 8 + (int)(lane >> 2), part = lane & 3;
+                const unsigned long long dst = __shfl_sync(0xffffffffu, mine, r);
+                const uint4 val =
+                    *reinterpret_cast<const uint4*>(ob + r * 64 + ((part ^ ((r >> 1) & 3)) * 16));
+                if (dst) reinterpret_cast<uint4*>(dst)[part] = val;
+              }
+              __syncwarp();
               continue;
             }
           }
@@ -1687,7 +1735,17 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
       return launch_tc<512, 4, EPI_BIAS_COMBINE, 2, 8>(ma, mb2, a, tiles512, st);
     }
 #endif
-    if (CG == 2) return launch_tc<256, 6, EPI_BIAS_COMBINE, 2, 8>(ma, mb, a, max_tiles, st);
+    if (CG == 2)
+      return push_base ? launch_tc<256, 6, EPI_COMBINE_PUSH, 2, 8>(ma, mb, a, max_tiles, st)
+                       : launch_tc<256, 6, EPI_BIAS_COMBINE, 2, 8>(ma, mb, a, max_tiles, st);
+    if (push_base != nullptr) {  // EP push return on 1-CTA tiles (small groups)
+      switch (BN) {
+        case 32: return launch_tc<32, 8, EPI_COMBINE_PUSH, 1, 4>(ma, mb, a, max_tiles, st);
+        case 64: return launch_tc<64, 8, EPI_COMBINE_PUSH, 1, 8>(ma, mb, a, max_tiles, st);
+        case 128: return launch_tc<128, 6, EPI_COMBINE_PUSH, 1, 8>(ma, mb, a, max_tiles, st);
+        default: return launch_tc<256, 4, EPI_COMBINE_PUSH, 1, 4>(ma, mb, a, max_tiles, st);
+      }
+    }
     switch (BN) {
       case 32: return launch_tc<32, 8, EPI_BIAS_COMBINE, 1, 4>(ma, mb, a, max_tiles, st);
       case 64: return launch_tc<64, 8, EPI_BIAS_COMBINE, 1, 8>(ma, mb, a, max_tiles, st);
