@@ -371,8 +371,12 @@ class MoeLayer:
                 self._pipe = HostPipeline(self._forward_dev, self.M, self.dtype, self.device)
             xh = x if x.dtype == self.dtype else x.to(self.dtype)
             oh = out if (out is not None and not out.is_cuda) else None
-            return self._pipe(xh, oh, logits_out=logits_out, timer=timer)
-        return self._forward_dev(x, out, logits_out, timer)
+            with torch.cuda.device(self.device):
+                return self._pipe(xh, oh, logits_out=logits_out, timer=timer)
+        # kernels launch on the current device: make it this layer's (one process
+        # may drive layers on several GPUs)
+        with torch.cuda.device(self.device):
+            return self._forward_dev(x, out, logits_out, timer)
 
     def _forward_dev(self, x: torch.Tensor, out: torch.Tensor | None = None,
                      logits_out: torch.Tensor | None = None, timer=None) -> torch.Tensor:

@@ -43,8 +43,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     extra = []
-    if os.environ.get("MOE_BUILD_EXPERIMENTAL") == "1":  # opt-in variants (A/B runs only)
-        extra.append("-DMOE_EXPERIMENTAL_BN512_COMBINE")
     cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
            *sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -851,7 +851,11 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         // kSplit: a whole part is read into registers (kCP x 32 columns) and its
         // TMEM handed straight back, so the MMAs refill it while the epilogue
         // computes (the GELU drain is MUFU-bound and outlasts the MMA run-ahead)
-        constexpr int kRB = kSplit ? kCP : 2;
+        // kStream (the fused combine on 256 x 512 tiles): not MUFU-bound, so chunks
+        // are read one at a time and each part is handed back after its last chunk
+        // (32 accumulator registers instead of a whole part: no spills)
+        constexpr bool kStream = kSplit && is_combine<EPI>();
+        constexpr int kRB = kSplit ? (kStream ? 1 : kCP) : 2;
         uint32_t r[kRB][32];
         if constexpr (!kSplit) tmem_ld_32x32b_x32(t_lane + tmem_col(0), r[0]);
 #pragma unroll
@@ -861,7 +865,19 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           if constexpr (kLoadX) {
             if (c + 1 < kChunks) load_x(c + 1, xbuf[(c + 1) & 1]);
           }
-          if constexpr (kSplit) {
+          if constexpr (kStream) {
+            if (c % kCP == 0 && c > 0) {
+              mbar_wait(&tfull[c / kCP], acc_phase);
+              tc_fence_after();
+            }
+            tmem_ld_32x32b_x32(t_lane + tmem_col(c), r[0]);
+            tmem_ld_wait_regs(r[0]);
+            if (c % kCP == kCP - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster(&tempty[c / kCP], pl);
+            }
+          } else if constexpr (kSplit) {
             if (c % kCP == 0) {
               if (c > 0) {
                 mbar_wait(&tfull[c / kCP], acc_phase);
@@ -1719,22 +1735,19 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
     }
   }
   if (act == 2) {  // fused combine epilogue
-#ifdef MOE_EXPERIMENTAL_BN512_COMBINE
-    // 256 x 512 fused-combine tiles: measured 2% slower than 256 x 256 and they
-    // spill (684 B stores / 1152 B loads), so they are only compiled on request
-    // (MOE_BUILD_EXPERIMENTAL=1 at build time) and then selected by MOE_BN512=1
+    // 256 x 512 fused-combine tiles (MOE_COMBINE_BN512=1): the epilogue streams
+    // chunk by chunk (kStream), 25% fewer operand bytes per flop than 256 x 256
     static const int bn512c = [] {
-      const char* v = getenv("MOE_BN512");
+      const char* v = getenv("MOE_COMBINE_BN512");
       return v ? atoi(v) : 0;
     }();
-    if (CG == 2 && bn512c == 1 && (N % 512) == 0) {
+    if (CG == 2 && bn512c == 1 && push_base == nullptr && (N % 512) == 0) {
       CUtensorMap mb2;
       rc = make_map(&mb2, B, b_rows, K, 128);
       if (rc) return rc;
       const int64_t tiles512 = (int64_t)G * ((max_group_rows + tm - 1) / tm) * ((N + 511) / 512);
       return launch_tc<512, 4, EPI_BIAS_COMBINE, 2, 8>(ma, mb2, a, tiles512, st);
     }
-#endif
     if (CG == 2)
       return push_base ? launch_tc<256, 6, EPI_COMBINE_PUSH, 2, 8>(ma, mb, a, max_tiles, st)
                        : launch_tc<256, 6, EPI_BIAS_COMBINE, 2, 8>(ma, mb, a, max_tiles, st);
