@@ -71,6 +71,8 @@ def parse():
                     help="reference arm: skip the C1 / C2 / C3 CPU legs")
     ap.add_argument("--sustained-s", type=float, default=2.0,
                     help="seconds of the power-capped steady-state loop (0: skip)")
+    ap.add_argument("--l2-flush", default="auto", choices=["auto", "on", "off"],
+                    help="read-only L2 flush between timed steps (auto: when x fits L2)")
     ap.add_argument("--no-strong", action="store_true",
                     help="N>1: skip the C3 strong-scaling point (64K tokens in total)")
     ap.add_argument("--no-decode", action="store_true")
@@ -569,6 +571,9 @@ def run_gpu(args):
     # GEMM2 epilogues store the combined rows straight into it over NVLink)
     out = torch.empty_like(x) if world == 1 else None
     flush, l2_note = l2_policy(S, M, E, residual)
+    if args.l2_flush != "auto":  # diagnostic override (e.g. gate timing after a clean L2)
+        flush = args.l2_flush == "on"
+        l2_note += f"; overridden: flush {'on' if flush else 'off'}"
     flush_buf = torch.empty(512 * 2 ** 20 // 2, dtype=torch.float16, device=dev).fill_(0) \
         if flush else None
     clocks = Clocks(local) if rank == 0 else None
@@ -776,17 +781,16 @@ def run_gpu(args):
                                 "frac_hbm": round(gbs / hbm, 3)}
     for sd, d in decode_roof.items():
         d["frac_hbm"] = round(d["GB_s"] / hbm, 3)
-    cfg = bench_config(args.workload, S, world)
-    if world > 1:
-        cfg.update(transport=layer.transport, schedule=layer.schedule,
-                   chunks=getattr(layer, "chunks", 1))
+    cfg = bench_config(args.workload, S, world)  # identical dict in the reference arm
+    ep_cfg = ({"transport": layer.transport, "schedule": layer.schedule,
+               "chunks": getattr(layer, "chunks", 1)} if world > 1 else None)
     line = {
         "metric": metric_name(args.workload),
         "value": S * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "p50_ms": p50,
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": cfg, "l2": l2_note,
+        "config": cfg, "ep": ep_cfg, "l2": l2_note,
         "roofline": roof,
         "sustained": sustained,
         "strong_scaling": strong,
