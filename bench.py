@@ -788,6 +788,8 @@ def run_gpu(args):
         "metric": metric_name(args.workload),
         "value": S * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "p50_ms": p50,
+        "step_ms": {"min": min(per), "max": max(per), "first": per[0],
+                    "all": [round(v, 4) for v in per] if len(per) <= 50 else None},
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": cfg, "ep": ep_cfg, "l2": l2_note,

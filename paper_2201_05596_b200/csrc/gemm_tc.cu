@@ -528,7 +528,24 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         } else if (lane == 0) {
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
-          if constexpr (kNI > 1) {
+          if constexpr (kNI > 1 && CL == 4) {
+            // 256 x 512 pair tiles, two pairs per cluster on the two m-blocks of one
+            // (group, n-block): the 512-column weight tile is shared - every CTA loads
+            // half of its B rows of each MMA and multicasts them to its counterpart
+            // in the other pair (L2->SM weight bytes halved again)
+            tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
+            constexpr int kHalf = 128 / CLP;  // B rows per multicast box
+#pragma unroll
+            for (int i = 0; i < kNI; ++i)
+              tma_load_2d_cg2_mc(sb + i * 128 * BK * 2 + pair * kHalf * BK * 2, &map_b,
+                                 &full[stage], kb * BK,
+                                 w * args.N + nb * BN + i * 256 + (int)cta * 128 + (int)pair * kHalf,
+                                 (uint16_t)((1u << cta) | (1u << (cta + 2))));
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+            else
+              mbar_arrive_cluster(&full[stage], pl);
+          } else if constexpr (kNI > 1) {
             tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
 #pragma unroll
             for (int i = 0; i < kNI; ++i)  // B rows of MMA i: [nb*BN + i*256 + cta*128, +128)
@@ -1797,10 +1814,51 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
       return v ? atoi(v) : 3;
     }();
     const bool long_launch = 2.0 * (double)G * (double)max_group_rows * N * K >= 1e12;
+    static const int cluster4 = [] {
+      const char* v = getenv("MOE_CLUSTER4");
+      return v ? atoi(v) : 0;
+    }();
     if ((bn512 == 1 || (bn512 >= 2 && !gelu) || (bn512 == 3 && long_launch)) && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
         (N % 512) == 0 && make_map_out3d(&md, D, G, per_group, N) == 0) {
       // 256 x 512 pair tiles; TMEM holds one accumulator, handed over in two halves
       CUtensorMap mb2;
+      if ((cluster4 == 3 || cluster4 == 4) && a_gather == nullptr) {
+        // MOE_CLUSTER4=3: two such pairs per 4-CTA cluster sharing the weight tile
+        // by multicast (512 x 512 per cluster; only whole-GPC clusters fit: 33 of
+        // them, 132 SMs). =4: plus a 2-CTA instance on the SMs they leave (each
+        // pair runs both 256-row halves of a 512 x 512 tile), both instances
+        // pulling tiles from one dynamic counter on two streams
+        CUtensorMap mb64;
+        rc = make_map(&mb64, B, b_rows, K, 64);
+        if (rc) return rc;
+        a.tma_store = 1;
+        const int64_t tiles4 = (int64_t)G * ((max_group_rows + 2 * tm - 1) / (2 * tm)) * ((N + 511) / 512);
+        const int nclus = max_clusters4(gelu);
+        const int64_t left = num_sms() - 4 * (int64_t)nclus;
+        int* ctr = cluster4 == 4 ? dyn_counter(st, 0, 0, true) : nullptr;
+        if (ctr == nullptr || left < 2) {
+          a.tile_counter = nullptr;  // the pairs of a cluster move in step (static schedule)
+          return gelu ? launch_tc<512, 4, EPI_BIAS_GELU, 2, 8, 4>(ma, mb64, a, tiles4, st, &md)
+                      : launch_tc<512, 4, EPI_BIAS, 2, 8, 4>(ma, mb64, a, tiles4, st, &md);
+        }
+        rc = make_map(&mb2, B, b_rows, K, 128);
+        if (rc) return rc;
+        a.tile_counter = ctr;
+        cudaStream_t side;
+        cudaEvent_t fork, join;
+        if (!side_stream(&side, &fork, &join)) return MOE_EINVAL;
+        cudaEventRecord(fork, st);
+        cudaStreamWaitEvent(side, fork, 0);
+        int r1 = gelu ? launch_tc<512, 4, EPI_BIAS_GELU, 2, 8, 4>(ma, mb64, a, tiles4, st, &md)
+                      : launch_tc<512, 4, EPI_BIAS, 2, 8, 4>(ma, mb64, a, tiles4, st, &md);
+        int r2 = gelu ? launch_tc<512, 4, EPI_BIAS_GELU, 2, 8, 2, 2>(ma, mb2, a, tiles4, side, &md,
+                                                                       left - left % 2)
+                      : launch_tc<512, 4, EPI_BIAS, 2, 8, 2, 2>(ma, mb2, a, tiles4, side, &md,
+                                                               left - left % 2);
+        cudaEventRecord(join, side);
+        cudaStreamWaitEvent(st, join, 0);
+        return r1 ? r1 : r2;
+      }
       rc = make_map(&mb2, B, b_rows, K, 128);
       if (rc) return rc;
       a.tma_store = 1;
@@ -1808,10 +1866,6 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
       return gelu ? launch_tc<512, 4, EPI_BIAS_GELU, 2, 8>(ma, mb2, a, tiles512, st, &md)
                   : launch_tc<512, 4, EPI_BIAS, 2, 8>(ma, mb2, a, tiles512, st, &md);
     }
-    static const int cluster4 = [] {
-      const char* v = getenv("MOE_CLUSTER4");
-      return v ? atoi(v) : 0;
-    }();
     if (cluster4 == 2 && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
         (N % 8) == 0 && a_gather == nullptr && make_map_out3d(&md, D, G, per_group, N) == 0) {
       // hybrid: the 4-CTA clusters that fit (weight tile multicast across two pairs)
