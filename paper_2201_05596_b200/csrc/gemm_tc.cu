@@ -127,6 +127,10 @@ struct GemmArgs {
   // row_src[r]'s buffer push_base[row_src[r]] at row row_token[r] (over NVLink)
   void* const* push_base;
   const int32_t* row_src;
+  // gate (CTA pairs): pair p owns the 128-row routing tiles [p*R/P, (p+1)*R/P), run
+  // two per pair tile; an odd last one runs on the leader's rows only (the peer
+  // skips its A load) - balanced to one routing tile instead of one pair tile
+  int gate_bal;
   int tma_store;    // EPI_BIAS / EPI_BIAS_GELU: whole-box TMA stores through map_d
   int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
   int raster;       // tile order (see tile_at)
@@ -343,7 +347,19 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   // CTAs' queues; every other role reads its CTA's queue and frees the slot.
   const bool dyn = args.tile_counter != nullptr;
   int claimed = -1;  // writer (lane 0): the tile claimed one iteration ahead
+  // balanced gate: "tiles" are first routing tiles (128-row units) of this pair's range
+  const bool gbal = EPI == EPI_GATE && CL == CG && args.gate_bal != 0;
+  int g_lo = 0, g_hi = 0;
+  if (gbal) {
+    const int R = (int)((args.S + BM - 1) / BM);
+    g_lo = (int)((int64_t)work_id * R / work_stride);
+    g_hi = (int)((int64_t)(work_id + 1) * R / work_stride);
+  }
   auto fetch = [&](int it, bool writer) -> int {
+    if (gbal) {
+      const int t = g_lo + 2 * it;
+      return t < g_hi ? t : -1;
+    }
     if (!dyn) {
       const int t = tile_at(it);
       return t < total_tiles ? t : -1;
@@ -397,11 +413,13 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       const int tile = cur;
       const int it = vit / SUB;
       if (tile < 0) break;
-      int mb, nb;
-      decode(tile, g, mb, nb);
+      int mb = 0, nb = 0;
+      if (!gbal) decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
-      const int mrow = mb * TMC + (int)(pair * SUB + sub) * TM;  // this pair's m-block
+      const int mrow = gbal ? tile * BM : mb * TMC + (int)(pair * SUB + sub) * TM;  // this pair's m-block
+      // balanced gate, odd last routing tile: only the leader's 128 rows are this pair's
+      const bool g_half = gbal && tile + 1 >= g_hi;
       // shared-MLP groups of a Residual-MoE launch read x (map_a2) instead of the
       // dispatched expert buffer
       const bool use_a2 = args.has_a2 && g >= args.a2_group;
@@ -420,7 +438,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           grow[i] = lr < rg ? args.a_gather[rs + lr] : 0;
         }
       }
-      if (args.prefetch && !dyn && lane == 0) {
+      if (args.prefetch && !dyn && !gbal && lane == 0) {
         // Warm L2 with the NEXT tile's streamed operand while this one runs: the
         // smem ring alone keeps too few DRAM bytes in flight per SM to hide the
         // loaded HBM latency (x for the gate, the weights for the expert GEMMs).
@@ -567,10 +585,12 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             else
               mbar_arrive_cluster(&full[stage], pl);
           } else if constexpr (CG == 2) {
-            tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
+            // (balanced gate half tile: the peer's A rows belong to the next pair - not
+            // loaded; the MMA's rows for them are garbage the epilogue ignores)
+            if (!(g_half && cta == 1)) tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
             tma_load_2d_cg2(sb, &map_b, &full[stage], kb * BK, b_row);
             if (leader)
-              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes - (g_half ? L::kABytes : 0));
             else
               mbar_arrive_cluster(&full[stage], pl);
           } else {
@@ -745,13 +765,15 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       if (sub == 0) cur = fetch(vit / SUB, false);
       const int tile = cur;
       if (tile < 0) break;
-      int mb, nb;
-      decode(tile, g, mb, nb);
+      int mb = 0, nb = 0;
+      if (!gbal) decode(tile, g, mb, nb);
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int64_t rows_g = args.rows ? args.rows[g] : args.rows_const;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
-      const int64_t local_row = (int64_t)mb * TMC + sub * TM + row_in_tile;
-      const bool valid = local_row < rows_g;
+      const int64_t local_row =
+          gbal ? (int64_t)tile * BM + row_in_tile : (int64_t)mb * TMC + sub * TM + row_in_tile;
+      const bool g_skip = gbal && cta == 1 && tile + 1 >= g_hi;  // the next pair's rows
+      const bool valid = local_row < rows_g && !g_skip;
       const int64_t out_row = rs + local_row;
       bool kzero = false;  // weight gradient of a group with no rows: zeros, TMEM not written
       if constexpr (kMN) kzero = (args.k_rows ? args.k_rows[g] : args.k_rows_const) == 0;
@@ -1345,8 +1367,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           args.local_rank[t * k] = r0;
           if (k == 2) args.local_rank[t * k + 1] = r1;
         }
-        const int64_t tile_row0 = (int64_t)mb * TMC + pair * TM + cta * BM;  // this CTA's routing tile
-        if (tile_row0 < args.S)
+        const int64_t tile_row0 = gbal ? (int64_t)tile * BM + cta * BM
+                                       : (int64_t)mb * TMC + pair * TM + cta * BM;  // this CTA's routing tile
+        if (tile_row0 < args.S && !g_skip)
           for (int e = tid; e < E; e += 128)
             args.tile_counts[tile_row0 / kRouteTile * E + e] =
                 wc[e] + wc[E + e] + wc[2 * E + e] + wc[3 * E + e];
@@ -2124,6 +2147,14 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   a.tile_counts = tile_counts;
   a.probsum = probsum;
   a.prefetch = prefetch_mode() & 1 ? 1 : 0;
+  // MOE_GATE_BAL=1: per-pair routing-tile ranges balanced to one 128-row routing
+  // tile. Parity-green but measured slower (C3 gate 60.4 vs 58.4 us, L2 flushed:
+  // profiles/r2_gate_bal.log) - a half pair tile costs nearly a full one - so off
+  static const int gate_bal = [] {
+    const char* v = getenv("MOE_GATE_BAL");
+    return v ? atoi(v) : 0;
+  }();
+  a.gate_bal = (CG == 2 && CLP == 1) ? gate_bal : 0;
   const int64_t tiles = (S + (int64_t)BM * CG * CLP - 1) / ((int64_t)BM * CG * CLP);
   if (CLP == 2)
     return BN == 128 ? launch_tc<128, 8, EPI_GATE, 2, 4, 4>(ma, mb, a, tiles, st)
