@@ -2116,7 +2116,11 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   // E >= 128: 2-CTA clusters (M=256 tokens per pair, each CTA loads half of W_g^T per
   // stage) so the smem ring holds more x bytes in flight per SM (the gate is
   // HBM-latency bound: 66 -> ~52 us at C3 measured for the smaller-B configs)
-  const int CG = BN >= 128 ? 2 : 1;
+  static const int gate_cg1 = [] {  // MOE_GATE_CG1=1: 1-CTA tiles for E in (64, 128]
+    const char* v = getenv("MOE_GATE_CG1");
+    return v ? atoi(v) : 0;
+  }();
+  const int CG = (BN >= 128 && !(gate_cg1 && BN == 128)) ? 2 : 1;
   // MOE_GATE_CL4=1 (E > 64): 4-CTA clusters, two pairs on consecutive 256-token
   // blocks sharing W_g^T by TMA multicast (each CTA loads a quarter per stage).
   // Stand-alone gate 59.4 -> 57.3 us at C3 (L2 flushed) but the layer is 0.4%
@@ -2162,7 +2166,9 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   switch (BN) {
     case 32: return launch_tc<32, 8, EPI_GATE>(ma, mb, a, tiles, st);
     case 64: return launch_tc<64, 8, EPI_GATE>(ma, mb, a, tiles, st);
-    case 128: return launch_tc<128, 8, EPI_GATE, 2, 4>(ma, mb, a, tiles, st);
+    case 128:
+      return CG == 1 ? launch_tc<128, 6, EPI_GATE, 1, 4>(ma, mb, a, tiles, st)
+                     : launch_tc<128, 8, EPI_GATE, 2, 4>(ma, mb, a, tiles, st);
     default: return launch_tc<256, 6, EPI_GATE, 2, 4>(ma, mb, a, tiles, st);
   }
 }
