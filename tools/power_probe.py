@@ -47,6 +47,19 @@ def g2t():
               0 | _lib.MOE_GEMM_PAD_SCRATCH, st)
 
 
+S_tok = G * cap
+row_token = torch.randperm(S_tok, device="cuda").to(torch.int32)
+row_prob = torch.rand(S_tok, device="cuda")
+xres = torch.randn(S_tok, M, device="cuda").to(torch.bfloat16)
+outc = torch.empty_like(xres)
+
+
+def g2c():  # the layer's GEMM2: bias + gate-prob scale + residual combine in the epilogue
+    _lib.call("moe_grouped_gemm_bf16_combine", h.data_ptr(), G * cap, F, w2.data_ptr(), G * M, M,
+              b2.data_ptr(), G, None, cap, None, cap, None, cap, row_token.data_ptr(),
+              row_prob.data_ptr(), xres.data_ptr(), outc.data_ptr(), None, st)
+
+
 def c1():
     torch.matmul(x, wa, out=h)
 
@@ -111,6 +124,9 @@ SETS = {
             ("grouped_gemm2", g2), ("grouped_gemm2_tma", g2t), ("cublas_bmm2_per_expert_w", bb2),
             ("grouped_gemm1_gelu", g1), ("grouped_gemm1_gelu_tma", g1t)),
     "ab": (("grouped_gemm1_gelu_tma", g1t), ("grouped_gemm2_tma", g2t)),
+    "cmp": (("grouped_gemm1_gelu_tma", g1t), ("cublas_bmm1_per_expert_w", bb1),
+            ("grouped_gemm2_fused_combine", g2c), ("grouped_gemm2_tma", g2t),
+            ("cublas_bmm2_per_expert_w", bb2)) * 2,
 }
 for name, fn in SETS[os.environ.get("PROBE_SET", "all")]:
     probe(name, fn)
