@@ -73,6 +73,8 @@ def parse():
                     help="seconds of the power-capped steady-state loop (0: skip)")
     ap.add_argument("--l2-flush", default="auto", choices=["auto", "on", "off"],
                     help="read-only L2 flush between timed steps (auto: when x fits L2)")
+    ap.add_argument("--drop-variant", action="store_true",
+                    help="N=1: SURVEY 8(d)'s drop-exercising logits (~45%% dropped at C3)")
     ap.add_argument("--no-strong", action="store_true",
                     help="N>1: skip the C3 strong-scaling point (64K tokens in total)")
     ap.add_argument("--no-decode", action="store_true")
@@ -451,7 +453,7 @@ def peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def make_layer(S, M, E, k, cf, dev, seed=0, residual=False):
+def make_layer(S, M, E, k, cf, dev, seed=0, residual=False, drop_variant=False):
     import torch
 
     from paper_2201_05596_b200 import arch as A
@@ -463,6 +465,11 @@ def make_layer(S, M, E, k, cf, dev, seed=0, residual=False):
     F = 4 * M
     # random-init weights of the named architecture: N(0,1)*0.1, zero biases (arch.py:347-365)
     gw = torch.randn(M, E, device=dev, generator=gen) * 0.1
+    if drop_variant:
+        # SURVEY 8(d) drop-exercising variant: unit-scale logits plus a per-expert
+        # bias N(0, 0.5^2), entering through the constant input feature x[:, 0] = 1
+        gw = torch.randn(M, E, device=dev, generator=gen) * M ** -0.5
+        gw[0] = torch.randn(E, device=dev, generator=gen) * 0.5
     w1 = torch.randn(E, M, F, device=dev, generator=gen, dtype=torch.bfloat16) * 0.1
     w2 = torch.randn(E, F, M, device=dev, generator=gen, dtype=torch.bfloat16) * 0.1
     zb1, zb2 = torch.zeros(1, F, device=dev), torch.zeros(1, M, device=dev)
@@ -563,9 +570,11 @@ def run_gpu(args):
                                      gpus_per_node=gpn if args.schedule == "hierarchical" else None,
                                      chunks=args.chunks, comm_sms=args.comm_sms)
     else:
-        layer = make_layer(S, M, E, k, cf, dev, residual=residual)
+        layer = make_layer(S, M, E, k, cf, dev, residual=residual, drop_variant=args.drop_variant)
     gen = torch.Generator(device=dev).manual_seed(1 + rank)
     x = torch.randn(S, M, device=dev, generator=gen).to(torch.bfloat16)
+    if args.drop_variant:
+        x[:, 0] = 1.0
     # synthetic routing with unbiased logits: ~4% drops at C3
     # (expert-parallel layers return their own output: for k=1 layers the owners'
     # GEMM2 epilogues store the combined rows straight into it over NVLink)
@@ -769,8 +778,11 @@ def run_gpu(args):
     A_r = kept_rank
     T_r = (S + 127) // 128
     epad = max(32, 1 << (E - 1).bit_length())
+    # dispatch: kept rows read + written; the k=1 fused dispatch also copies every
+    # fully dropped token to out (its skip connection), so it moves every row once
+    fused_k1 = world == 1 and k == 1 and not residual
     comp_bytes = {"gate": S * M * 2 + epad * M * 2 + S * k * 12 + T_r * E * 4,
-                  "dispatch": 2 * A_r * M * 2,
+                  "dispatch": (2 * S * M * 2) if fused_k1 else 2 * A_r * M * 2,
                   "combine": (A_r * M + 2 * S * M + (S * M if residual else 0)) * 2}
     components = {}
     for name, nbytes in comp_bytes.items():
@@ -802,6 +814,7 @@ def run_gpu(args):
         "components": components,
         "train_step": train,
         "kept_assignments_per_gpu": kept_rank,
+        "drop_variant": bool(args.drop_variant),
         "cpu_baseline": cpu,
         "e2e": {"value": S * world / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": S * M * 2, "d2h_bytes_per_step": S * M * 2},
