@@ -253,6 +253,15 @@ MOE_DEV void bulk_wait_group_read() {
 }
 MOE_DEV void bulk_wait_group_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Programmatic dependent launch: a kernel launched with the programmatic stream
+// serialization attribute may be scheduled while its predecessor drains (its
+// prologue - barrier init, TMEM alloc - overlaps the predecessor's tail). It must
+// not touch global memory before pdl_wait() (returns once every prerequisite grid
+// has completed and its memory is visible); pdl_trigger() lets this kernel's own
+// dependents be scheduled. Both are no-ops without the attribute.
+MOE_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+MOE_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // global writes of the async proxy (TMA stores) ordered with the generic proxy
 MOE_DEV void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");

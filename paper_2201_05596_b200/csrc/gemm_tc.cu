@@ -251,8 +251,10 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   const int work_id = blockIdx.x / CL, work_stride = gridDim.x / CL;
   if constexpr (CG == 2) cluster_sync();  // both CTAs resident before the paired TMEM alloc
 
+  pdl_trigger();  // (programmatic dependent launch: see common.cuh)
   // ---- per-CTA tile table: tile_start[g] = sum_{g'<g} ceil(rows/TM) * n_blocks
   if (warp == 0) {
+    pdl_wait();  // the group row counts come from the previous kernel
     const int per = (G + 31) / 32;
     const int g0 = lane * per;
     int local = 0;
@@ -313,6 +315,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   else
     __syncthreads();
   tc_fence_after();
+  pdl_wait();  // every role: no global access before the predecessor grid completed
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = tile_start[G];
 
@@ -1636,13 +1639,15 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   cfg.blockDim = dim3(threads_for<EW, EPI>());
   cfg.dynamicSmemBytes = L::kTotal;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
   if constexpr (CL > 2) {
     // 4-CTA clusters must fit whole GPCs: size the persistent grid to what can be resident
     static std::atomic<int> clusters_by_dev[kMaxDevices];

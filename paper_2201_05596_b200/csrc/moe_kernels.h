@@ -8,6 +8,26 @@
 
 namespace moe {
 
+// MOE_PDL (default 0): launch the forward hot-path kernels with programmatic
+// dependent launch (see pdl_wait / pdl_trigger in common.cuh)
+bool pdl_on();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 int launch_topk_gate(const void* logits, int dtype, int64_t S, int E, int k, int32_t* ids,
                      void* gate_probs, void* probs, cudaStream_t st);
 

@@ -16,6 +16,17 @@
 
 namespace moe {
 
+// MOE_PDL=1: programmatic dependent launch for the forward hot-path kernels.
+// Parity-green (full GPU suite) but no gain: C2 / C4 within noise, C3 burst
+// 17.1 vs 17.5 M tok/s (profiles/r2_ab_pdl.log) - off by default
+bool pdl_on() {
+  static const bool on = [] {
+    const char* v = getenv("MOE_PDL");
+    return v ? atoi(v) != 0 : false;
+  }();
+  return on;
+}
+
 // ============================================================ top-k gate
 // One warp per token row. Lane l owns columns l, l+32, ... (coalesced).
 constexpr int kNoExpert = 0x7fffffff;
@@ -159,6 +170,8 @@ __global__ void plan_scan_kernel(const int32_t* __restrict__ tile_counts, int64_
                                  int32_t* __restrict__ tile_offsets, int32_t* __restrict__ totals,
                                  int32_t* __restrict__ kept) {
   __shared__ int part[32][33];
+  pdl_trigger();
+  pdl_wait();
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int e = blockIdx.x * 32 + tx;
   const int64_t chunk = (T + 31) / 32;
@@ -300,6 +313,8 @@ __global__ void blelloch_down_kernel(double* tree, int64_t m, int64_t d) {
 // TPW tokens per warp (32/TPW lanes each), as in combine_kernel.
 template <typename V, int TPW = 1>
 __global__ void scatter_kernel(ScatterArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int LPT = 32 / TPW;  // lanes per token
   const int lane = threadIdx.x & (LPT - 1);
   const int64_t slots_total = (int64_t)gridDim.x * (blockDim.x >> 5) * TPW;
@@ -544,6 +559,8 @@ __global__ void __launch_bounds__(256, 3) combine_tb_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nv = M / NV;  // 16-B vectors per row
   const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  pdl_trigger();
+  pdl_wait();
   // persistent grid (resident blocks only): block b owns the contiguous token range
   // [b*S/grid, (b+1)*S/grid), so the work is balanced to a token, not to a batch
   const int64_t lo = (int64_t)blockIdx.x * S / gridDim.x;
@@ -721,7 +738,7 @@ int launch_plan(const int32_t* ids, int64_t S, int k, int E, int64_t cap, const 
   }
   if (scan) {
     dim3 blk(32, 32);
-    plan_scan_kernel<<<(E + 31) / 32, blk, 0, st>>>(tile_counts, T, E, cap, base, tile_offsets,
+    launch_pdl(plan_scan_kernel, dim3((E + 31) / 32), blk, 0, st, tile_counts, T, E, cap, base, tile_offsets,
                                                     totals, kept);
   }
   if (do_slots && S > 0) {
@@ -787,10 +804,12 @@ int launch_scatter(const ScatterArgs& args, cudaStream_t st) {
   const int tpw = tpw_env ? tpw_env : (args.peer_buf != nullptr ? 4 : 2);
   if (tpw == 4 && args.row_bytes % 16 == 0) {
     const int g4 = (g + 3) / 4;
-    scatter_kernel<uint4, 4><<<g4 > 0 ? g4 : 1, threads, 0, st>>>(args);
+    return (int)launch_pdl(scatter_kernel<uint4, 4>, dim3(g4 > 0 ? g4 : 1), dim3(threads), 0, st,
+                           args);
   } else if (tpw == 2 && args.row_bytes % 16 == 0) {
     const int g2 = (g + 1) / 2;
-    scatter_kernel<uint4, 2><<<g2 > 0 ? g2 : 1, threads, 0, st>>>(args);
+    return (int)launch_pdl(scatter_kernel<uint4, 2>, dim3(g2 > 0 ? g2 : 1), dim3(threads), 0, st,
+                           args);
   } else if (args.row_bytes % 16 == 0)
     scatter_kernel<uint4><<<g, threads, 0, st>>>(args);
   else if (args.row_bytes % 8 == 0)
@@ -845,8 +864,8 @@ static void combine_vec(bool expert_order, int g, int threads, cudaStream_t st, 
     auto kern = combine_tb_kernel<T, P, EO_, TB_, (sizeof(T) == 2 ? 2 : 4), SH_>;               \
     const int64_t res = resident_blocks(kern, 256);                                             \
     const int gb = (int)(blocks < res ? blocks : res);                                          \
-    kern<<<gb, 256, 0, st>>>((const T*)y, S, M, k, E, cap, ids, slots, row_index, (const P*)gp, \
-                             (const T*)x, (const T*)shared, (T*)out);                           \
+    launch_pdl(kern, dim3(gb), dim3(256), 0, st, (const T*)y, S, M, k, E, cap, ids, slots,      \
+               row_index, (const P*)gp, (const T*)x, (const T*)shared, (T*)out);               \
   }
     const bool sh = shared != nullptr;
     if (tb == 16) {
