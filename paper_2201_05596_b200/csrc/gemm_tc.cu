@@ -131,6 +131,7 @@ struct GemmArgs {
   // two per pair tile; an odd last one runs on the leader's rows only (the peer
   // skips its A load) - balanced to one routing tile instead of one pair tile
   int gate_bal;
+  int coal_store;   // fused combine: stage each 32 x 32 chunk in smem, store 4 lanes per row
   int tma_store;    // EPI_BIAS / EPI_BIAS_GELU: whole-box TMA stores through map_d
   int stream_hint;  // epilogue outputs / residual reads are touched once: evict them first
   int raster;       // tile order (see tile_at)
@@ -193,7 +194,7 @@ constexpr int out_stage_bytes() {
   return (EPI == EPI_WGRAD ||
           (CG == 2 && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID)))
              ? EW * out_bufs<BN>() * 2048
-             : ((CG == 2 && EPI == EPI_COMBINE_PUSH && BN <= 256) ? EW * 2048 : 0);
+             : ((CG == 2 && is_combine<EPI>()) ? EW * 2048 : 0);
 }
 
 // CL = cluster size: CG (one CTA pair per cluster) or 2*CG = 4: two pairs run the
@@ -887,17 +888,30 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               xq[q] = args.stream_hint ? ld_global_nc_hint(xs + q, pol_stream) : __ldg(xs + q);
           }
         };
-        uint4 xbuf[2][4];
-        if constexpr (kLoadX) load_x(0, xbuf[0]);
+        // kStream (the fused combine on 256 x 512 tiles): not MUFU-bound, so chunks
+        // are read one at a time and each part is handed back after its last chunk
+        // (32 accumulator registers instead of a whole part: no spills)
+        constexpr bool kStream = kSplit && is_combine<EPI>();
+        // kStream: a part's residual chunks are all
+        // loaded before the part's accumulator is awaited (the loads hide under the
+        // MMAs; per-chunk prefetch left ~3 us of latency per part exposed, stalling
+        // the MMA run-ahead); otherwise prefetched one chunk ahead
+        constexpr int kXB = kStream ? kCP : 2;
+        uint4 xbuf[kXB][4];
+        auto xslot = [&](int c) -> int { return kStream ? c % kCP : c & 1; };
+        if constexpr (kLoadX) {
+          if constexpr (kStream) {
+#pragma unroll
+            for (int e = 0; e < kCP; ++e) load_x(e, xbuf[e]);
+          } else {
+            load_x(0, xbuf[0]);
+          }
+        }
         // TMEM loads double-buffered across 32-column chunks: the load of
         // chunk c+1 is in flight while chunk c is biased, activated and stored.
         // kSplit: a whole part is read into registers (kCP x 32 columns) and its
         // TMEM handed straight back, so the MMAs refill it while the epilogue
         // computes (the GELU drain is MUFU-bound and outlasts the MMA run-ahead)
-        // kStream (the fused combine on 256 x 512 tiles): not MUFU-bound, so chunks
-        // are read one at a time and each part is handed back after its last chunk
-        // (32 accumulator registers instead of a whole part: no spills)
-        constexpr bool kStream = kSplit && is_combine<EPI>();
         constexpr int kRB = kSplit ? (kStream ? 1 : kCP) : 2;
         uint32_t r[kRB][32];
         if constexpr (!kSplit) tmem_ld_32x32b_x32(t_lane + tmem_col(0), r[0]);
@@ -905,11 +919,15 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         for (int c = 0; c < kChunks; ++c) {
           const int cl = chunk_col(c);  // column inside the tile
           const int col0 = nb * BN + cl;
-          if constexpr (kLoadX) {
+          if constexpr (kLoadX && !kStream) {
             if (c + 1 < kChunks) load_x(c + 1, xbuf[(c + 1) & 1]);
           }
           if constexpr (kStream) {
             if (c % kCP == 0 && c > 0) {
+              if constexpr (kLoadX) {
+#pragma unroll
+                for (int e = 0; e < kCP; ++e) load_x(c + e, xbuf[e]);
+              }
               mbar_wait(&tfull[c / kCP], acc_phase);
               tc_fence_after();
             }
@@ -977,9 +995,13 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           // EP push return: rows go to scattered peer rows, so the warp stages its
           // 32 x 32 chunk in smem and stores it 4 lanes per row (full 64-B row
           // segments per NVLink write instead of 16-B pieces of 32 different rows)
-          constexpr bool kCoalOK = out_stage_bytes<EPI, EW, CG, BN>() > 0 && BN <= 256 &&
-                                   (EPI == EPI_BIAS || EPI == EPI_COMBINE_PUSH);
-          const bool coal = kCoalOK && args.push_base != nullptr && vec_ok && col0 + 32 <= N;
+          // (also the local fused combine, whose rows are scattered over `out` by token:
+          // 4x fewer store transactions, and the 256 x 512 tile's epilogue fits the
+          // MMA run-ahead)
+          constexpr bool kCoalOK = out_stage_bytes<EPI, EW, CG, BN>() > 0 &&
+                                   ((EPI == EPI_BIAS && BN <= 256) || is_combine<EPI>());
+          const bool coal = kCoalOK && (args.push_base != nullptr || (is_combine<EPI>() && args.coal_store)) &&
+                            vec_ok && col0 + 32 <= N;
           if (col0 >= N) continue;
           if (!valid && !(kTmaEpi && args.tma_store) && !coal) continue;
           float v[32];
@@ -1092,7 +1114,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           }
           if constexpr (EPI == EPI_GELU_BWD) {  // no bias: D = dH, times gelu'(a)
             if (vec_ok && col0 + 32 <= N) {
-              const __nv_bfloat16* ab = reinterpret_cast<const __nv_bfloat16*>(xbuf[c & 1]);
+              const __nv_bfloat16* ab = reinterpret_cast<const __nv_bfloat16*>(xbuf[xslot(c)]);
 #pragma unroll
               for (int i = 0; i < 32; ++i)
                 v[i] = __uint_as_float(r[c % kRB][i]) * gelu_tanh_grad_fast(__bfloat162float(ab[i]));
@@ -1125,7 +1147,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
               }
             }
             if (vec_ok && col0 + 32 <= N) {
-              const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(xbuf[c & 1]);
+              const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(xbuf[xslot(c)]);
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = fmaf(prob, v[i], __bfloat162float(xb[i]));
             } else {
@@ -1751,6 +1773,11 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
   a.a_gather = a_gather;
   a.push_base = push_base;
   a.row_src = row_src;
+  static const int coal = [] {  // MOE_COMBINE_COAL (default 1): coalesced combine stores
+    const char* v = getenv("MOE_COMBINE_COAL");
+    return v ? atoi(v) : 1;
+  }();
+  a.coal_store = coal;
   a.tile_counter = dyn_counter(st, K, N);
   a.stream_hint = stream_hint;
   a.raster = raster;
