@@ -57,3 +57,26 @@ def test_random_backward(i):
     cf = float(r.uniform(0.4, 1.6))
     res = bool(r.random() < 0.4)
     check(S, M, E, k, cf, res)
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_random_layer_odd_width(i):
+    """d_model a multiple of 8 but not of 32: the epilogues' partial 32-column
+    chunks (scalar tails of the combine / Residual-MoE epilogues, BN 64 / 128 /
+    256 tiles with a ragged last block)."""
+    r = np.random.default_rng(3000 + i)
+    M = int(r.choice([40, 72, 136, 200]))
+    E = int(r.integers(2, 20))
+    k = int(r.choice([1, 2]))
+    S = int(r.integers(300, 2500))
+    cf = float(r.uniform(0.5, 2.0))
+    res = bool(i % 2)
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, residual=res, gating=GatingConfig(E, k, cf))
+    p = rounded_params(spec, 91 + i, torch.bfloat16)
+    x64 = torch.randn(S, M, generator=torch.Generator().manual_seed(50 + i)).to(torch.bfloat16)
+    x64 = x64.double().numpy()
+    layer, x, out, logits = run_layer(spec, p, x64, torch.bfloat16, fuse=bool(i % 3))
+    lg, _ = check_routing(layer, logits, spec, S)
+    ex, sh = oracle_args(p)
+    want = O.forward_layer_with_logits(x64, lg, ex, sh, E, k, cf)
+    close(out.float().cpu().numpy(), want, 2e-2)
