@@ -150,9 +150,11 @@ constexpr int acc_stages() {
   return 2 * BN <= 512 ? 2 : 1;
 }
 
-template <int BN, int STAGES, int CG, int OUT = 0>
+// MS: 128-row A sub-tiles per CTA sharing each B stage (the gate: two pair tiles
+// of tokens against one W_g^T stage, so the weight is streamed half as often)
+template <int BN, int STAGES, int CG, int OUT = 0, int MS = 1>
 struct Smem {
-  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kABytes = MS * BM * BK * 2;
   static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOff = STAGES * kStageBytes;
@@ -166,9 +168,9 @@ struct Smem {
   static constexpr int kTotal = kOutOff + OUT + 1024;                    // +1024 align slack
 };
 
-template <int BN>
+template <int BN, int MS = 1>
 constexpr uint32_t tmem_cols() {
-  return (acc_stages<BN>() * BN) < 32 ? 32 : (acc_stages<BN>() * BN);
+  return (acc_stages<BN * MS>() * BN * MS) < 32 ? 32 : (acc_stages<BN * MS>() * BN * MS);
 }
 
 // EPI_WGRAD stages each warp's 32 x 32 output chunk in smem (2 x 2 KB per warp,
@@ -202,15 +204,17 @@ constexpr int out_stage_bytes() {
 // loading half of it and multicasting to its counterpart in the other pair.
 // SUB: m-blocks a pair runs per scheduled tile (1, or 2 for the 2-CTA instance that
 // shares a cluster-4 launch's tile pool, whose tiles span two m-blocks).
-template <int BN, int STAGES, int EPI, int CG, int EW, int CL = CG, int SUB = 1>
+template <int BN, int STAGES, int EPI, int CG, int EW, int CL = CG, int SUB = 1, int MS = 1>
 __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_d, GemmArgs args,
                         const __grid_constant__ CUtensorMap map_a2) {
-  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>()>;
-  constexpr int TM = BM * CG;  // rows per tile
-  constexpr int AS = acc_stages<BN>();
+  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>(), MS>;
+  static_assert(MS == 1 || (EPI == EPI_GATE && CL == CG && SUB == 1), "A sub-tiles: gate pairs only");
+  constexpr int TM = BM * CG;  // rows per MMA (a pair tile)
+  constexpr int AS = acc_stages<BN * MS>();
+  constexpr int kAccW = BN * MS;  // TMEM columns per accumulator stage
   // MMAs per K step: N <= 256 per tcgen05.mma; a BN = 512 pair tile issues two,
   // each CTA holding 128 B rows of each (two 16 KB halves of its B stage)
   constexpr int kNI = (CG == 2 && BN > 256) ? BN / 256 : 1;
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   const int n_blocks = (args.N + BN - 1) / BN;
   static_assert(CL == CG || (CG == 2 && CL == 4), "cluster = one pair or two pairs");
   constexpr int CLP = CL / CG;  // CTA pairs per cluster
-  constexpr int TMC = TM * CLP * SUB;  // rows per scheduled tile
+  constexpr int TMC = TM * CLP * SUB * MS;  // rows per scheduled tile
   const uint32_t qrank = CL > 1 ? cluster_ctarank() : 0;
   const uint32_t cta = qrank % CG;    // rank inside the CTA pair
   const uint32_t pair = qrank / CG;   // pair inside the cluster
@@ -300,9 +304,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     }
     __syncwarp();
     if constexpr (CG == 2)
-      tmem_alloc_cg2(tmem_slot, tmem_cols<BN>());
+      tmem_alloc_cg2(tmem_slot, tmem_cols<BN, MS>());
     else
-      tmem_alloc(tmem_slot, tmem_cols<BN>());
+      tmem_alloc(tmem_slot, tmem_cols<BN, MS>());
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
@@ -591,7 +595,11 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           } else if constexpr (CG == 2) {
             // (balanced gate half tile: the peer's A rows belong to the next pair - not
             // loaded; the MMA's rows for them are garbage the epilogue ignores)
-            if (!(g_half && cta == 1)) tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
+            if (!(g_half && cta == 1)) {
+#pragma unroll
+              for (int ms = 0; ms < MS; ++ms)  // sub-tile ms: the pair tile ms*TM rows on
+                tma_load_2d_cg2(sa + ms * BM * BK * 2, mA, &full[stage], kb * BK, a_row + ms * TM);
+            }
             tma_load_2d_cg2(sb, &map_b, &full[stage], kb * BK, b_row);
             if (leader)
               mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes - (g_half ? L::kABytes : 0));
@@ -696,7 +704,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       }
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
+      const uint32_t d_tmem = tmem_base + acc * kAccW;
       for (int kb = 0; kb < kb_end; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -714,7 +722,11 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
                               bdesc + (uint64_t)i * ((128 * BK * 2) >> 4) + kStep * kk, idesc,
                               (kb | kk) != 0);
             } else if constexpr (CG == 2) {
-              umma_bf16_cg2(d_tmem, adesc + kStep * kk, bdesc + kStep * kk, idesc, (kb | kk) != 0);
+#pragma unroll
+              for (int ms = 0; ms < MS; ++ms)
+                umma_bf16_cg2(d_tmem + ms * BN,
+                              adesc + (uint64_t)ms * ((BM * BK * 2) >> 4) + kStep * kk,
+                              bdesc + kStep * kk, idesc, (kb | kk) != 0);
             } else {
               umma_bf16(d_tmem, adesc + kStep * kk, bdesc + kStep * kk, idesc, (kb | kk) != 0);
             }
@@ -797,8 +809,8 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         const int rr = (c / kCP) * (kPW / 2) + (c % kCP) * 32;  // B row in CTA col_part
         return kSplit ? (rr / 128) * 256 + col_part * 128 + rr % 128 : (col_part * kChunks + c) * 32;
       };
-      const uint32_t t_lane = tmem_base + ((quarter * 32) << 16) + acc * BN;
-      const uint32_t t_addr = tmem_base + ((quarter * 32) << 16) + acc * BN +
+      const uint32_t t_lane = tmem_base + ((quarter * 32) << 16) + acc * kAccW;
+      const uint32_t t_addr0 = tmem_base + ((quarter * 32) << 16) + acc * kAccW +
                               (EPI != EPI_GATE ? col_part * kChunks * 32 : 0);
 
       if constexpr (EPI != EPI_GATE) {
@@ -1241,7 +1253,12 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       } else {
         // ---------------- gate epilogue: thread = token row, BN >= E columns
         const int E = args.E;
-        const int64_t t = out_row;  // single group: rows are tokens
+        // MS > 1: sub-tile ms = the pair tile ms*TM rows further, its accumulator
+        // ms*BN TMEM columns further (both sub-tiles shared every W_g^T stage)
+        for (int ms = 0; ms < MS; ++ms) {
+        const uint32_t t_addr = t_addr0 + ms * BN;
+        const int64_t t = out_row + ms * TM;  // single group: rows are tokens
+        const bool valid = local_row + ms * TM < rows_g && !g_skip;
         float b1 = -INFINITY, b2 = -INFINITY;
         int i1 = 0x7fffffff, i2 = 0x7fffffff;
 #pragma unroll 1
@@ -1341,7 +1358,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         // accumulator consumed: hand TMEM back to the MMA warp (the leader's, CG=2)
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0 && ms == MS - 1) {
           if constexpr (CG == 2)
             mbar_arrive_cluster(&tempty[acc], pl);
           else
@@ -1393,12 +1410,13 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           if (k == 2) args.local_rank[t * k + 1] = r1;
         }
         const int64_t tile_row0 = gbal ? (int64_t)tile * BM + cta * BM
-                                       : (int64_t)mb * TMC + pair * TM + cta * BM;  // this CTA's routing tile
+                                       : (int64_t)mb * TMC + pair * TM + ms * TM + cta * BM;  // this CTA's routing tile
         if (tile_row0 < args.S && !g_skip)
           for (int e = tid; e < E; e += 128)
             args.tile_counts[tile_row0 / kRouteTile * E + e] =
                 wc[e] + wc[E + e] + wc[2 * E + e] + wc[3 * E + e];
         named_bar_sync(1, 128);
+        }  // ms
       }
       if (++acc == AS) {
         acc = 0;
@@ -1474,9 +1492,9 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   if (warp == 1) {
     tc_fence_after();
     if constexpr (CG == 2)
-      tmem_dealloc_cg2(tmem_base, tmem_cols<BN>());
+      tmem_dealloc_cg2(tmem_base, tmem_cols<BN, MS>());
     else
-      tmem_dealloc(tmem_base, tmem_cols<BN>());
+      tmem_dealloc(tmem_base, tmem_cols<BN, MS>());
   }
 }
 
@@ -1638,13 +1656,14 @@ static cudaError_t ensure_smem_attr(Kern kern, int bytes, std::atomic<uint64_t>&
   return e;
 }
 
-template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4, int CL = CG, int SUB = 1>
+template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4, int CL = CG, int SUB = 1,
+          int MS = 1>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
                      int64_t max_tiles, cudaStream_t st, const CUtensorMap* md = nullptr,
                      int64_t grid_cap = 0, const CUtensorMap* ma2 = nullptr) {
-  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>()>;
+  using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>(), MS>;
   static_assert(L::kTotal <= 227 * 1024, "dynamic shared memory beyond the 227 KB per CTA");
-  auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW, CL, SUB>;
+  auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW, CL, SUB, MS>;
   static std::atomic<uint64_t> attr_done{0};
   {
     cudaError_t e = ensure_smem_attr(kern, L::kTotal, attr_done);
@@ -2191,6 +2210,16 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
     return v ? atoi(v) : 0;
   }();
   a.gate_bal = (CG == 2 && CLP == 1) ? gate_bal : 0;
+  // MOE_GATE_MS=2 (E in (64, 128], pairs): each CTA runs two 128-row sub-tiles against
+  // every W_g^T stage (512 tokens per pair tile): the weight crosses L2->SM half as often
+  static const int gate_ms = [] {
+    const char* v = getenv("MOE_GATE_MS");
+    return v ? atoi(v) : 1;
+  }();
+  if (gate_ms == 2 && CG == 2 && CLP == 1 && BN == 128 && !a.gate_bal) {
+    const int64_t tiles2 = (S + 4 * (int64_t)BM - 1) / (4 * (int64_t)BM);
+    return launch_tc<128, 5, EPI_GATE, 2, 4, 2, 1, 2>(ma, mb, a, tiles2, st);
+  }
   const int64_t tiles = (S + (int64_t)BM * CG * CLP - 1) / ((int64_t)BM * CG * CLP);
   if (CLP == 2)
     return BN == 128 ? launch_tc<128, 8, EPI_GATE, 2, 4, 4>(ma, mb, a, tiles, st)
