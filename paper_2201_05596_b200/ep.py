@@ -13,15 +13,19 @@ its own shard). One all-gather of the per-rank (E,) expert counts gives every
 rank those prefixes, so routing, slots and the dropped set are bit-identical
 to ``build_dispatch_plan`` run on the whole batch at any p.
 
-Two transports. "p2p" (k=1 layers, default): no collective on the data path -
-the dispatch kernel stores each kept row straight into its owner's receive
-buffer over NVLink (laid out [local expert][global slot], i.e. the single-GPU
-expert buffer), the owner's GEMM2 epilogue combines in place (x + p*y), and
-the source pulls its rows back with wide NVLink loads; a 2-line flag barrier
-(system-scope release/acquire) separates the phases, and the plan is computed
-on device from the all-gathered counts (no host sync).
+Two transports. "p2p" (default for the flat schedule, every layer kind): no
+collective on the data path - the counts are all-gathered over peer memory,
+the plan is computed on device (no host sync), the dispatch kernel stores each
+kept row straight into its owner's receive buffer over NVLink (laid out
+[local expert][global slot], i.e. the single-GPU expert buffer), and the
+owner's GEMM2 epilogue stores every row straight back to its source: k=1
+layers combined (x + p*y) into the source's output slot, k=2 / Residual-MoE
+expert rows into the source's return buffer, which the source combines
+locally (plus its replicated shared MLP). System-scope flag barriers separate
+the phases. (chunks > 1: the round-1 pipelined variant, owner-local combine
+and a source-side pull.)
 
-"nccl" (any k, shared MLP) - one all-to-all each way, flat (one NCCL
+"nccl" (any k, shared MLP; the hierarchical schedule) - one all-to-all each way, flat (one NCCL
 all_to_all_single) or, with schedule="hierarchical", the two-phase
 node/rail schedule of commsim.py:280-370 (exchange.py):
   send buffer on rank r : kept rows ordered (owner rank, expert, slot)
