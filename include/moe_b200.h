@@ -172,6 +172,9 @@ int moe_load_balance_loss_from_stats(const int32_t* counts, const float* probsum
  * whole 32-row boxes go out through TMA tensor stores (the expert buffers'
  * padding rows; without the flag D rows past rows[g] are never written). */
 #define MOE_GEMM_PAD_SCRATCH 0x100
+/* act flag: keep 256-column tiles (no 256 x 512 tiles) - the expert-parallel owner
+ * GEMM1, where the 512-column GELU tiles measured less even across ranks */
+#define MOE_GEMM_TILE256 0x200
 int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
                           int N, const float* bias, void* D, int num_groups,
                           const int32_t* row_start, int64_t row_stride, const int32_t* rows,
@@ -323,6 +326,14 @@ int moe_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap, 
                 int32_t* row_base, int32_t* seg_start, int32_t* seg_rows, int32_t* recv_rows,
                 void* stream);
 
+/* moe_ep_plan with the padded receive layout: local expert j owns rows
+ * [j*cap, (j+1)*cap), row = j*cap + global slot (the single-GPU expert buffer);
+ * seg_start[j] = j*cap. The owner's grouped GEMMs then run with a uniform group
+ * stride (row_start NULL, row_stride = cap). */
+int moe_ep_plan_padded(const int32_t* counts, int world, int rank, int E, int64_t cap,
+                       int32_t* slot_base, int32_t* row_base, int32_t* seg_start, int32_t* seg_rows,
+                       int32_t* recv_rows, void* stream);
+
 /* moe_ep_plan for C token chunks per rank (chunk c of rank s = its tokens
  * [c*S/C, (c+1)*S/C)): counts (world, C, E); outputs per chunk: slot_base
  * (C, E), row_base (C, E), seg_start / seg_rows (C, E/world), recv_rows (C);
@@ -376,10 +387,11 @@ int moe_dispatch_p2p(const void* x, int64_t S, int64_t row_bytes, int E, int k, 
  *    (x_r = x_rows[r], the dispatched token row), into the source's output;
  *  combine = 0: y = acc + b2, into the source's (S * k)-row return buffer, which
  *    the source then combines locally (moe_combine / moe_residual_gemm_bf16).
- * row_token / row_src / row_prob come from moe_dispatch_p2p with peer_src set. */
+ * row_token / row_src / row_prob come from moe_dispatch_p2p with peer_src set.
+ * Groups start at row_start[g] or, with row_start NULL, at g * row_stride. */
 int moe_grouped_gemm_bf16_push(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
                                int N, const float* bias, int num_groups, const int32_t* row_start,
-                               const int32_t* rows, const int32_t* weight_idx,
+                               int64_t row_stride, const int32_t* rows, const int32_t* weight_idx,
                                int64_t max_group_rows, int combine, const int32_t* row_token,
                                const float* row_prob, const int32_t* row_src,
                                void* const* push_base, const void* x_rows, void* stream);

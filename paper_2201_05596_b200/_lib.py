@@ -21,6 +21,7 @@ MOE_F32, MOE_BF16, MOE_F64 = 0, 1, 2
 MOE_ACT_NONE, MOE_ACT_GELU = 0, 1
 MOE_ACT_GELU_SAVE, MOE_ACT_GELU_BWD = 3, 4
 MOE_GEMM_PAD_SCRATCH = 0x100  # act flag: rows past each group's count are scratch
+MOE_GEMM_TILE256 = 0x200  # act flag: keep 256-column tiles
 ROUTE_TILE = 128
 MOE_EINVAL = -22
 
@@ -66,8 +67,9 @@ SIGNATURES = {
     "moe_ipc_allgather_i32": (_I, [_P, _I, _P, _I, _I, _P, _P, _P, _P, _P]),
     "moe_dispatch_p2p": (_I, [_P, _L, _L, _I, _I, _L, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P,
                               _P, _P, _P, _I, _P]),
-    "moe_grouped_gemm_bf16_push": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _P, _P, _L, _I, _P,
-                                        _P, _P, _P, _P, _P]),
+    "moe_grouped_gemm_bf16_push": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _L, _P, _P, _L, _I,
+                                        _P, _P, _P, _P, _P, _P]),
+    "moe_ep_plan_padded": (_I, [_P, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P]),
     "moe_grouped_gemm_bf16_combine_rows": (_I, [_P, _L, _I, _P, _L, _I, _P, _I, _P, _P, _P, _L,
                                                 _P, _P, _P, _P, _P]),
     "moe_pull_rows_p2p": (_I, [_L, _L, _I, _I, _P, _P, _I, _P, _P, _P]),

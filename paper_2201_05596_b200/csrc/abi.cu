@@ -216,8 +216,9 @@ int moe_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B, i
                           int64_t rows_const, const int32_t* weight_idx, int64_t max_group_rows,
                           int act, void* stream) {
   CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1);
-  const int pad_scratch = (act & MOE_GEMM_PAD_SCRATCH) ? 1 : 0;
-  act &= ~MOE_GEMM_PAD_SCRATCH;
+  // (bit 1 of pad_scratch carries MOE_GEMM_TILE256 to the launcher)
+  const int pad_scratch = ((act & MOE_GEMM_PAD_SCRATCH) ? 1 : 0) | ((act & MOE_GEMM_TILE256) ? 2 : 0);
+  act &= ~(MOE_GEMM_PAD_SCRATCH | MOE_GEMM_TILE256);
   CHECK(act == MOE_ACT_NONE || act == MOE_ACT_GELU);
   CHECK(max_group_rows >= 0 && rows_const >= 0);
   if (a_rows == 0 || max_group_rows == 0) return MOE_OK;

@@ -42,10 +42,14 @@ int comm_block_limit() { return t_comm_blocks; }
 // (C = 1: the single-GPU expert buffer without padding). Outputs per chunk c:
 // slot_base[c][e], row_base[c][e] (my first chunk-c row for e in its owner's
 // buffer), seg_start/seg_rows[c][j] (my buffer as an owner), recv_rows[c].
+// padded (C = 1 only): every local expert owns cap rows, row = e_loc * cap + global
+// slot - the single-GPU expert buffer's layout, so the owner's grouped GEMMs run
+// with a uniform group stride (TMA-store epilogues, 256 x 512 tiles)
 __global__ void ep_plan_kernel(const int32_t* __restrict__ counts, int world, int rank, int E,
                                int C, int64_t cap, int32_t* __restrict__ slot_base,
                                int32_t* __restrict__ row_base, int32_t* __restrict__ seg_start,
-                               int32_t* __restrict__ seg_rows, int32_t* __restrict__ recv_rows) {
+                               int32_t* __restrict__ seg_rows, int32_t* __restrict__ recv_rows,
+                               int padded) {
   extern __shared__ int kept[];  // [world][C][E], then chunk_off [world][C]
   int* chunk_off = kept + world * C * E;
   const int e_loc = E / world;
@@ -72,6 +76,23 @@ __global__ void ep_plan_kernel(const int32_t* __restrict__ counts, int world, in
     }
   }
   __syncthreads();
+  if (padded) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x)
+      row_base[e] = (int)((e % e_loc) * cap + slot_base[e]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t tot = 0;
+      for (int j = 0; j < e_loc; ++j) {
+        int64_t r = 0;
+        for (int s = 0; s < world; ++s) r += kept[s * E + rank * e_loc + j];
+        seg_start[j] = (int)(j * cap);
+        seg_rows[j] = (int)r;
+        tot += r;
+      }
+      recv_rows[0] = (int)tot;
+    }
+    return;
+  }
   for (int ce = threadIdx.x; ce < C * E; ce += blockDim.x) {
     const int c = ce / E, e = ce % E;
     const int o = e / e_loc, el = e % e_loc;
@@ -243,11 +264,11 @@ int launch_pull_rows(int64_t S, int64_t row_bytes, int k, int e_per_rank, const 
 
 int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int C, int64_t cap,
                    int32_t* slot_base, int32_t* row_base, int32_t* seg_start, int32_t* seg_rows,
-                   int32_t* recv_rows, cudaStream_t st) {
+                   int32_t* recv_rows, cudaStream_t st, int padded) {
   const size_t smem = ((size_t)world * C * E + (size_t)world * C) * sizeof(int);
-  if (smem > 48 * 1024) return MOE_EINVAL;
+  if (smem > 48 * 1024 || (padded && C != 1)) return MOE_EINVAL;
   ep_plan_kernel<<<1, 256, smem, st>>>(counts, world, rank, E, C, cap, slot_base, row_base,
-                                       seg_start, seg_rows, recv_rows);
+                                       seg_start, seg_rows, recv_rows, padded);
   return (int)cudaGetLastError();
 }
 
@@ -312,6 +333,16 @@ int moe_ep_plan(const int32_t* counts, int world, int rank, int E, int64_t cap, 
   CHECK(counts && slot_base && row_base && seg_start && seg_rows && recv_rows);
   return moe::launch_ep_plan(counts, world, rank, E, 1, cap, slot_base, row_base, seg_start,
                              seg_rows, recv_rows, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int moe_ep_plan_padded(const int32_t* counts, int world, int rank, int E, int64_t cap,
+                       int32_t* slot_base, int32_t* row_base, int32_t* seg_start, int32_t* seg_rows,
+                       int32_t* recv_rows, void* stream) {
+  CHECK(world >= 1 && rank >= 0 && rank < world && E >= world && E % world == 0 && cap >= 0);
+  CHECK((int64_t)(E / world) * cap < ((int64_t)1 << 31));
+  CHECK(counts && slot_base && row_base && seg_start && seg_rows && recv_rows);
+  return moe::launch_ep_plan(counts, world, rank, E, 1, cap, slot_base, row_base, seg_start,
+                             seg_rows, recv_rows, reinterpret_cast<cudaStream_t>(stream), 1);
 }
 
 int moe_ep_plan_chunked(const int32_t* counts, int world, int rank, int E, int chunks, int64_t cap,
@@ -411,19 +442,20 @@ int moe_grouped_gemm_bf16_combine_rows(const void* A, int64_t a_rows, int K, con
 
 int moe_grouped_gemm_bf16_push(const void* A, int64_t a_rows, int K, const void* B, int64_t b_rows,
                                int N, const float* bias, int num_groups, const int32_t* row_start,
-                               const int32_t* rows, const int32_t* weight_idx,
+                               int64_t row_stride, const int32_t* rows, const int32_t* weight_idx,
                                int64_t max_group_rows, int combine, const int32_t* row_token,
                                const float* row_prob, const int32_t* row_src,
                                void* const* push_base, const void* x_rows, void* stream) {
   CHECK(a_rows >= 0 && K >= 8 && K % 8 == 0 && N >= 1 && b_rows >= N && num_groups >= 1);
   CHECK(max_group_rows >= 0 && (combine == 0 || combine == 1));
   if (a_rows == 0 || max_group_rows == 0) return MOE_OK;
-  CHECK(A && B && row_start && rows && row_token && row_src && push_base);
+  CHECK(A && B && (row_start || row_stride > 0) && rows && row_token && row_src && push_base);
   if (combine) CHECK(row_prob && x_rows);
   // combine = 1: act 2 (EPI_BIAS_COMBINE, x = the receive row itself); 0: bias only
   return moe::launch_grouped_gemm_bf16(A, a_rows, K, B, b_rows, N, bias, nullptr, num_groups,
-                                       row_start, 0, rows, 0, weight_idx, max_group_rows,
-                                       combine ? 2 : 0, reinterpret_cast<cudaStream_t>(stream),
+                                       row_start, row_start ? 0 : row_stride, rows, 0, weight_idx,
+                                       max_group_rows, combine ? 2 : 0,
+                                       reinterpret_cast<cudaStream_t>(stream),
                                        row_token, row_prob, x_rows, nullptr, combine ? 1 : 0, 0,
                                        nullptr, push_base, row_src);
 }

@@ -1746,6 +1746,8 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
                              const int32_t* a_gather, void* const* push_base,
                              const int32_t* row_src) {
   if (G < 1 || G > kMaxGroups || K < 1 || N < 1 || (K % 8) != 0) return MOE_EINVAL;
+  const bool force256 = (pad_scratch & 2) != 0;  // MOE_GEMM_TILE256
+  pad_scratch &= 1;
   int BN = 256;
   if (N <= 32) BN = 32;
   else if (N <= 64) BN = 64;
@@ -1892,7 +1894,7 @@ int launch_grouped_gemm_bf16(const void* A, int64_t a_rows, int K, const void* B
       const char* v = getenv("MOE_CLUSTER4");
       return v ? atoi(v) : 0;
     }();
-    if ((bn512 == 1 || (bn512 >= 2 && !gelu) || (bn512 == 3 && long_launch)) && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
+    if (!force256 && (bn512 == 1 || (bn512 >= 2 && !gelu) || (bn512 == 3 && long_launch)) && tma_epi && pad_scratch && row_start == nullptr && per_group > 0 &&
         (N % 512) == 0 && make_map_out3d(&md, D, G, per_group, N) == 0) {
       // 256 x 512 pair tiles; TMEM holds one accumulator, handed over in two halves
       CUtensorMap mb2;

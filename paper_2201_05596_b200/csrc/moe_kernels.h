@@ -108,7 +108,7 @@ int gemm_cta_limit();
 int comm_block_limit();
 int launch_ep_plan(const int32_t* counts, int world, int rank, int E, int C, int64_t cap,
                    int32_t* slot_base, int32_t* row_base, int32_t* seg_start, int32_t* seg_rows,
-                   int32_t* recv_rows, cudaStream_t st);
+                   int32_t* recv_rows, cudaStream_t st, int padded = 0);
 int launch_pull_rows(int64_t S, int64_t row_bytes, int k, int e_per_rank, const int32_t* ids,
                      const int32_t* row_index, uint8_t* const* peer_rows, uint8_t* out,
                      cudaStream_t st);

@@ -535,7 +535,9 @@ class EPMoeLayer:
                   self.world, self.rank, st["peer_sig"].data_ptr(), st["signal"].data_ptr(),
                   self._epoch_dev.data_ptr(), st["err"].data_ptr(), stream)
         ph("plan")
-        _lib.call("moe_ep_plan", st["counts"].data_ptr(), self.world, self.rank, E, cap,
+        # padded receive layout (local expert j at rows [j*cap, (j+1)*cap)): the owner's
+        # GEMMs run with a uniform group stride, like the single-GPU expert buffers
+        _lib.call("moe_ep_plan_padded", st["counts"].data_ptr(), self.world, self.rank, E, cap,
                   st["slot_base"].data_ptr(), st["row_base"].data_ptr(),
                   st["seg_start"].data_ptr(), st["seg_rows"].data_ptr(),
                   st["recv_rows"].data_ptr(), stream)
@@ -554,21 +556,23 @@ class EPMoeLayer:
         self._barrier(st)
         G = self.E_loc
         if cap:
+            # padding rows are scratch: TMA-store epilogue; 256-column tiles (the
+            # 256 x 512 GELU tiles measured less even across ranks: the return
+            # barrier waited 0.13-0.36 ms for the slower one, 0.02-0.06 ms on 256)
             ph("gemm1")
             _lib.call("moe_grouped_gemm_bf16", st["recv"].data_ptr(), st["rmax"], M,
                       self.w1.data_ptr(), self.E_loc * F, F, self.b1.data_ptr(),
-                      st["h"].data_ptr(), G, st["seg_start"].data_ptr(), 0,
-                      st["seg_rows"].data_ptr(), 0, st["seg_w"].data_ptr(), cap,
-                      _lib.MOE_ACT_GELU, stream)
+                      st["h"].data_ptr(), G, None, cap, st["seg_rows"].data_ptr(), 0, None, cap,
+                      _lib.MOE_ACT_GELU | _lib.MOE_GEMM_PAD_SCRATCH | _lib.MOE_GEMM_TILE256,
+                      stream)
             # GEMM2 + bias (+ combine and residual for k=1), every row stored straight
             # back to its source rank over NVLink
             ph("gemm2_push")
             _lib.call("moe_grouped_gemm_bf16_push", st["h"].data_ptr(), st["rmax"], F,
-                      self.w2.data_ptr(), self.E_loc * M, M, self.b2.data_ptr(), G,
-                      st["seg_start"].data_ptr(), st["seg_rows"].data_ptr(),
-                      st["seg_w"].data_ptr(), cap, 1 if push1 else 0, st["row_token"].data_ptr(),
-                      st["row_prob"].data_ptr(), st["row_src"].data_ptr(), dest.data_ptr(),
-                      st["recv"].data_ptr(), stream)
+                      self.w2.data_ptr(), self.E_loc * M, M, self.b2.data_ptr(), G, None, cap,
+                      st["seg_rows"].data_ptr(), None, cap, 1 if push1 else 0,
+                      st["row_token"].data_ptr(), st["row_prob"].data_ptr(),
+                      st["row_src"].data_ptr(), dest.data_ptr(), st["recv"].data_ptr(), stream)
         if self.shared is not None and S:
             ph("shared_mlp1")  # the source's shared MLP, first half (replicated weights)
             sh = self.shared

@@ -112,7 +112,7 @@ def step(timers=None):
             cnt = counts.to(d)
             s["_cnt"] = cnt
             mark(r, "plan")
-            _lib.call("moe_ep_plan", cnt.data_ptr(), W, r, E, cap, s["slot_base"].data_ptr(),
+            _lib.call("moe_ep_plan_padded", cnt.data_ptr(), W, r, E, cap, s["slot_base"].data_ptr(),
                       s["row_base"].data_ptr(), s["seg_start"].data_ptr(), s["seg_rows"].data_ptr(),
                       s["recv_rows"].data_ptr(), st_)
             _lib.call("moe_plan_scan", s["tc"].data_ptr(), S, E, cap, s["slot_base"].data_ptr(),
@@ -132,12 +132,13 @@ def step(timers=None):
             st_ = _lib.stream_ptr()
             mark(r, "gemm1")
             _lib.call("moe_grouped_gemm_bf16", s["recv"].data_ptr(), rmax, M, s["w1"].data_ptr(), EL * F,
-                      F, s["b1"].data_ptr(), s["h"].data_ptr(), EL, s["seg_start"].data_ptr(), 0,
-                      s["seg_rows"].data_ptr(), 0, s["seg_w"].data_ptr(), cap, _lib.MOE_ACT_GELU, st_)
+                      F, s["b1"].data_ptr(), s["h"].data_ptr(), EL, None, cap,
+                      s["seg_rows"].data_ptr(), 0, None, cap,
+                      _lib.MOE_ACT_GELU | _lib.MOE_GEMM_PAD_SCRATCH, st_)
             mark(r, "gemm2_push")
             _lib.call("moe_grouped_gemm_bf16_push", s["h"].data_ptr(), rmax, F, s["w2"].data_ptr(),
-                      EL * M, M, s["b2"].data_ptr(), EL, s["seg_start"].data_ptr(),
-                      s["seg_rows"].data_ptr(), s["seg_w"].data_ptr(), cap, 1,
+                      EL * M, M, s["b2"].data_ptr(), EL, None, cap,
+                      s["seg_rows"].data_ptr(), None, cap, 1,
                       s["row_token"].data_ptr(), s["row_prob"].data_ptr(), s["row_src"].data_ptr(),
                       s["peer_out"].data_ptr(), s["recv"].data_ptr(), st_)
             mark(r, "end")
