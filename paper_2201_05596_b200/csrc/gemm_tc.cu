@@ -446,6 +446,15 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           grow[i] = lr < rg ? args.a_gather[rs + lr] : 0;
         }
       }
+      if (args.prefetch && !dyn && gbal && lane == 0) {
+        // balanced gate: the next routing-tile pair of this pair's range (an odd last
+        // routing tile is the leader's alone)
+        const int nt = tile + 2;
+        if (nt < g_hi && (cta == 0 || nt + 1 < g_hi)) {
+          const int pa = (nt + (int)cta) * BM;
+          for (int kb = 0; kb < num_kb; ++kb) tma_prefetch_l2_2d(&map_a, kb * BK, pa);
+        }
+      }
       if (args.prefetch && !dyn && !gbal && lane == 0) {
         // Warm L2 with the NEXT tile's streamed operand while this one runs: the
         // smem ring alone keeps too few DRAM bytes in flight per SM to hide the
@@ -1139,7 +1148,10 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             }
           }
           if constexpr (is_combine<EPI>()) {
-            if (args.D != nullptr) {  // training: also keep y = acc + b2 (row layout) for backward
+            // training: also keep y = acc + b2 (row layout) for backward (valid rows
+            // only: with coalesced stores every lane of the warp reaches this point, and
+            // a tile's rows past the group's count may lie in the next group's block)
+            if (args.D != nullptr && valid) {
               __nv_bfloat16* yrow = args.D + out_row * N;
               if (vec_ok && col0 + 32 <= N) {
                 uint4* yd = reinterpret_cast<uint4*>(yrow + col0);
@@ -2206,7 +2218,9 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
   a.prefetch = prefetch_mode() & 1 ? 1 : 0;
   // MOE_GATE_BAL=1: per-pair routing-tile ranges balanced to one 128-row routing
   // tile. Parity-green but measured slower (C3 gate 60.4 vs 58.4 us, L2 flushed:
-  // profiles/r2_gate_bal.log) - a half pair tile costs nearly a full one - so off
+  // profiles/r2_gate_bal.log, with the next-tile L2 prefetch as well:
+  // profiles/r2_gate_wave_probe.log) - each SM streams x at a capped rate, so a
+  // half pair tile (the leader's 128 rows) takes as long as a full one - so off
   static const int gate_bal = [] {
     const char* v = getenv("MOE_GATE_BAL");
     return v ? atoi(v) : 0;

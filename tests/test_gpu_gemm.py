@@ -56,6 +56,48 @@ def test_grouped_gemm_bf16(K, N, act, pad):
         assert torch.isnan(d[2 * cap + 129:3 * cap].float()).all()
 
 
+@pytest.mark.parametrize("K,N", [(1024, 2048), (512, 1024), (136, 200)])
+def test_grouped_gemm_bf16_combine_keeps_y_in_bounds(K, N):
+    """Fused-combine GEMM2 of the training forward (train.py:119-122): out[token] =
+    x[token] + p * (A W^T + b) for every kept row, y = A W^T + b kept for backward.
+    Rows past a group's count are never written, neither in out nor in y - a
+    second 256-row tile of group 0 overhangs group 1's block (cap 300)."""
+    torch.manual_seed(K + 7 * N)
+    G, cap = 5, 300
+    rows = [300, 0, 129, 1, 257]
+    S = sum(rows)
+    a = (torch.randn(G * cap, K, device="cuda") * 0.5).to(torch.bfloat16)
+    w_t = (torch.randn(G * N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(G, N, device="cuda") * 0.1
+    x = torch.randn(S, N, device="cuda").to(torch.bfloat16)
+    perm = torch.randperm(S, device="cuda").to(torch.int32)
+    row_token = torch.full((G * cap,), -1, dtype=torch.int32, device="cuda")
+    row_prob = torch.rand(G * cap, device="cuda")
+    n = 0
+    for g, r in enumerate(rows):
+        row_token[g * cap:g * cap + r] = perm[n:n + r]
+        n += r
+    out = torch.full((S, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    y = torch.full((G * cap, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    rows_t = torch.tensor(rows, dtype=torch.int32, device="cuda")
+    _lib.call("moe_grouped_gemm_bf16_combine", a.data_ptr(), G * cap, K, w_t.data_ptr(), G * N, N,
+              bias.data_ptr(), G, None, cap, rows_t.data_ptr(), 0, None, cap,
+              row_token.data_ptr(), row_prob.data_ptr(), x.data_ptr(), out.data_ptr(),
+              y.data_ptr(), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    ref = _ref(a, w_t, bias, rows, [g * cap for g in range(G)], list(range(G)), 0, N)
+    for g, want in ref.items():
+        sl = slice(g * cap, g * cap + rows[g])
+        tol = 2e-2 * (want.abs().max().item() + 1.0)
+        assert (y[sl].float() - want).abs().max().item() <= tol, g
+        tok = row_token[sl].long()
+        want_out = x[tok].float() + row_prob[sl, None] * want
+        assert (out[tok].float() - want_out).abs().max().item() <= tol, g
+        assert torch.isnan(y[g * cap + rows[g]:(g + 1) * cap].float()).all(), g
+    assert torch.isnan(y[cap:2 * cap].float()).all()  # group 1: no rows
+    assert not torch.isnan(out.float()).any()  # every token is some kept row
+
+
 def test_grouped_gemm_bf16_weight_index_and_row_start():
     torch.manual_seed(0)
     K, N = 512, 512
