@@ -426,15 +426,18 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       const int64_t rs = args.row_start ? args.row_start[g] : (int64_t)g * args.row_stride;
       const int w = args.weight_idx ? args.weight_idx[g] : g;
       const int mrow = gbal ? tile * BM : mb * TMC + (int)(pair * SUB + sub) * TM;  // this pair's m-block
+      // (the per-tile TMA coordinates are made warp-uniform with a lane-0 shuffle, so
+      // ptxas keeps the issue path on uniform registers: no per-load R2UR waterfall)
       // balanced gate, odd last routing tile: only the leader's 128 rows are this pair's
-      const bool g_half = gbal && tile + 1 >= g_hi;
+      const bool g_half = __shfl_sync(0xffffffffu, (int)(gbal && tile + 1 >= g_hi), 0) != 0;
       // shared-MLP groups of a Residual-MoE launch read x (map_a2) instead of the
       // dispatched expert buffer
-      const bool use_a2 = args.has_a2 && g >= args.a2_group;
+      const bool use_a2 = __shfl_sync(0xffffffffu, (int)(args.has_a2 && g >= args.a2_group), 0) != 0;
       const CUtensorMap* mA = use_a2 ? &map_a2 : &map_a;
       const int64_t rs_a = use_a2 ? (int64_t)(g - args.a2_group) * args.row_stride : rs;
-      const int a_row = (int)(rs_a + (int64_t)mrow + cta * BM);
-      const int b_row = w * args.N + nb * BN + cta * (BN / CG);
+      const int a_row = __shfl_sync(0xffffffffu, (int)(rs_a + (int64_t)mrow + cta * BM), 0);
+      const int b_base = __shfl_sync(0xffffffffu, w * args.N + nb * BN, 0);
+      const int b_row = b_base + cta * (BN / CG);
       // gather mode: this lane's 4 source rows of the CTA's 128-row A tile (rows past
       // the group's count read row 0: their outputs are padding)
       int grow[4] = {0, 0, 0, 0};
@@ -560,7 +563,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
                         grow[3]);
             if (lane == 0) tma_load_2d(sb, &map_b, &full[stage], kb * BK, b_row);
           }
-        } else if (lane == 0) {
+        } else {  // warp-uniform: every lane runs this, one elected lane issues (*_e)
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           if constexpr (kNI > 1 && CL == 4) {
@@ -568,56 +571,56 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             // (group, n-block): the 512-column weight tile is shared - every CTA loads
             // half of its B rows of each MMA and multicasts them to its counterpart
             // in the other pair (L2->SM weight bytes halved again)
-            tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
+            tma_load_2d_cg2_e(sa, mA, &full[stage], kb * BK, a_row);
             constexpr int kHalf = 128 / CLP;  // B rows per multicast box
 #pragma unroll
             for (int i = 0; i < kNI; ++i)
-              tma_load_2d_cg2_mc(sb + i * 128 * BK * 2 + pair * kHalf * BK * 2, &map_b,
+              tma_load_2d_cg2_mc_e(sb + i * 128 * BK * 2 + pair * kHalf * BK * 2, &map_b,
                                  &full[stage], kb * BK,
-                                 w * args.N + nb * BN + i * 256 + (int)cta * 128 + (int)pair * kHalf,
+                                 b_base + i * 256 + (int)cta * 128 + (int)pair * kHalf,
                                  (uint16_t)((1u << cta) | (1u << (cta + 2))));
             if (leader)
-              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+              mbar_arrive_expect_tx_e(&full[stage], CG * L::kStageBytes);
             else
-              mbar_arrive_cluster(&full[stage], pl);
+              mbar_arrive_cluster_e(&full[stage], pl);
           } else if constexpr (kNI > 1) {
-            tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
+            tma_load_2d_cg2_e(sa, mA, &full[stage], kb * BK, a_row);
 #pragma unroll
             for (int i = 0; i < kNI; ++i)  // B rows of MMA i: [nb*BN + i*256 + cta*128, +128)
-              tma_load_2d_cg2(sb + i * 128 * BK * 2, &map_b, &full[stage], kb * BK,
-                              w * args.N + nb * BN + i * 256 + (int)cta * 128);
+              tma_load_2d_cg2_e(sb + i * 128 * BK * 2, &map_b, &full[stage], kb * BK,
+                              b_base + i * 256 + (int)cta * 128);
             if (leader)
-              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+              mbar_arrive_expect_tx_e(&full[stage], CG * L::kStageBytes);
             else
-              mbar_arrive_cluster(&full[stage], pl);
+              mbar_arrive_cluster_e(&full[stage], pl);
           } else if constexpr (CL == 4) {
             // weight tile shared by both pairs: load my half of my 128 B rows and
             // multicast it to my counterpart in the other pair (same cta index)
-            tma_load_2d_cg2(sa, mA, &full[stage], kb * BK, a_row);
+            tma_load_2d_cg2_e(sa, mA, &full[stage], kb * BK, a_row);
             constexpr int kHalf = BN / CG / CLP;  // B rows per multicast box
-            tma_load_2d_cg2_mc(sb + pair * kHalf * BK * 2, &map_b, &full[stage], kb * BK,
+            tma_load_2d_cg2_mc_e(sb + pair * kHalf * BK * 2, &map_b, &full[stage], kb * BK,
                                b_row + pair * kHalf, (uint16_t)((1u << cta) | (1u << (cta + 2))));
             if (leader)
-              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes);
+              mbar_arrive_expect_tx_e(&full[stage], CG * L::kStageBytes);
             else
-              mbar_arrive_cluster(&full[stage], pl);
+              mbar_arrive_cluster_e(&full[stage], pl);
           } else if constexpr (CG == 2) {
             // (balanced gate half tile: the peer's A rows belong to the next pair - not
             // loaded; the MMA's rows for them are garbage the epilogue ignores)
             if (!(g_half && cta == 1)) {
 #pragma unroll
               for (int ms = 0; ms < MS; ++ms)  // sub-tile ms: the pair tile ms*TM rows on
-                tma_load_2d_cg2(sa + ms * BM * BK * 2, mA, &full[stage], kb * BK, a_row + ms * TM);
+                tma_load_2d_cg2_e(sa + ms * BM * BK * 2, mA, &full[stage], kb * BK, a_row + ms * TM);
             }
-            tma_load_2d_cg2(sb, &map_b, &full[stage], kb * BK, b_row);
+            tma_load_2d_cg2_e(sb, &map_b, &full[stage], kb * BK, b_row);
             if (leader)
-              mbar_arrive_expect_tx(&full[stage], CG * L::kStageBytes - (g_half ? L::kABytes : 0));
+              mbar_arrive_expect_tx_e(&full[stage], CG * L::kStageBytes - (g_half ? L::kABytes : 0));
             else
-              mbar_arrive_cluster(&full[stage], pl);
+              mbar_arrive_cluster_e(&full[stage], pl);
           } else {
-            mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-            tma_load_2d(sa, mA, &full[stage], kb * BK, a_row);
-            tma_load_2d(sb, &map_b, &full[stage], kb * BK, b_row);
+            mbar_arrive_expect_tx_e(&full[stage], L::kStageBytes);
+            tma_load_2d_e(sa, mA, &full[stage], kb * BK, a_row);
+            tma_load_2d_e(sb, &map_b, &full[stage], kb * BK, b_row);
           }
         }
         __syncwarp();
@@ -628,7 +631,10 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (leader CTA only; lane 0 issues, whole warp waits)
+    // ===================== MMA issuer (leader CTA only). The whole warp runs the
+    // loop with warp-uniform values and one elected lane issues each tcgen05 op
+    // (the *_e helpers), so descriptors stay in uniform registers
+    const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
     constexpr uint32_t idesc = kMN ? make_idesc_bf16_mn(TM, BN) : make_idesc_bf16(TM, BN / kNI);
     // K step of one MMA (16 elements): +32 B inside the swizzle line (K-major) or
     // two 8-row groups (+2048 B, MN-major); descriptor units are 16 B
@@ -642,7 +648,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     int cur = -1;
     for (int vit = 0; leader; ++vit) {
       if (vit % SUB == 0) cur = fetch(vit / SUB, false);
-      const int tile = cur;
+      const int tile = __shfl_sync(0xffffffffu, cur, 0);
       if (tile < 0) break;
       int kb_end = num_kb;
       if constexpr (kMN) {
@@ -650,6 +656,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         decode(tile, g, mb_, nb_);
         const int64_t kg = args.k_rows ? args.k_rows[g] : args.k_rows_const;
         kb_end = (int)((kg + BK - 1) / BK);  // 0 for an empty group: the epilogue writes zeros
+        kb_end = __shfl_sync(0xffffffffu, kb_end, 0);
       }
       if constexpr (kSplit) {
         // BN = 512 pair tile, TMEM full: the accumulator is handed over in kParts
@@ -665,19 +672,17 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           tc_fence_after();
         };
         auto mma_part = [&](int kb, int j) {
-          if (lane == 0) {
-            const uint8_t* sa = smem + ((s0 + kb) % STAGES) * L::kStageBytes;
-            const uint64_t adesc = make_sdesc_sw128(sa);
-            const uint64_t bdesc =
-                make_sdesc_sw128(sa + L::kABytes) + (uint64_t)j * (((kPW / 2) * BK * 2) >> 4);
+          const uint8_t* sa = smem + ((s0 + kb) % STAGES) * L::kStageBytes;
+          const uint64_t adesc = make_sdesc_sw128(sa);
+          const uint64_t bdesc =
+              make_sdesc_sw128(sa + L::kABytes) + (uint64_t)j * (((kPW / 2) * BK * 2) >> 4);
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)
-              umma_bf16_cg2(tmem_base + j * kPW, adesc + kStep * kk, bdesc + kStep * kk, idesc_p,
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16_cg2_e(tmem_u + j * kPW, adesc + kStep * kk, bdesc + kStep * kk, idesc_p,
                             (kb | kk) != 0);
-          }
         };
         auto release = [&](int kb) {
-          if (lane == 0) umma_commit_cg2(&empty[(s0 + kb) % STAGES], CL == 4 ? 0xF : 0x3);
+          umma_commit_cg2_e(&empty[(s0 + kb) % STAGES], CL == 4 ? 0xF : 0x3);
         };
         constexpr int kRA = STAGES - 1;
         const int ra = kb_end < kRA ? kb_end : kRA;
@@ -703,7 +708,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             mma_part(kb, j);
             if (j == kParts - 1) release(kb);
           }
-          if (lane == 0) umma_commit_cg2(&tfull[j], (uint16_t)(0x3u << pl));
+          umma_commit_cg2_e(&tfull[j], (uint16_t)(0x3u << pl));
         }
         __syncwarp();
         stage = (s0 + kb_end) % STAGES;
@@ -713,51 +718,45 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       }
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * kAccW;
+      const uint32_t d_tmem = tmem_u + acc * kAccW;
       for (int kb = 0; kb < kb_end; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (lane == 0) {
-          const uint8_t* sa = smem + stage * L::kStageBytes;
-          const uint8_t* sb = sa + L::kABytes;
-          const uint64_t adesc = kMN ? make_sdesc_sw128_mn(sa) : make_sdesc_sw128(sa);
-          const uint64_t bdesc = kMN ? make_sdesc_sw128_mn(sb) : make_sdesc_sw128(sb);
+        const uint8_t* sa = smem + stage * L::kStageBytes;
+        const uint8_t* sb = sa + L::kABytes;
+        const uint64_t adesc = kMN ? make_sdesc_sw128_mn(sa) : make_sdesc_sw128(sa);
+        const uint64_t bdesc = kMN ? make_sdesc_sw128_mn(sb) : make_sdesc_sw128(sb);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            if constexpr (kNI > 1) {
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          if constexpr (kNI > 1) {
 #pragma unroll
-              for (int i = 0; i < kNI; ++i)  // B half i = 128 rows x 128 B further (>>4: +1024)
-                umma_bf16_cg2(d_tmem + i * 256, adesc + kStep * kk,
+            for (int i = 0; i < kNI; ++i)  // B half i = 128 rows x 128 B further (>>4: +1024)
+              umma_bf16_cg2_e(d_tmem + i * 256, adesc + kStep * kk,
                               bdesc + (uint64_t)i * ((128 * BK * 2) >> 4) + kStep * kk, idesc,
                               (kb | kk) != 0);
-            } else if constexpr (CG == 2) {
+          } else if constexpr (CG == 2) {
 #pragma unroll
-              for (int ms = 0; ms < MS; ++ms)
-                umma_bf16_cg2(d_tmem + ms * BN,
+            for (int ms = 0; ms < MS; ++ms)
+              umma_bf16_cg2_e(d_tmem + ms * BN,
                               adesc + (uint64_t)ms * ((BM * BK * 2) >> 4) + kStep * kk,
                               bdesc + kStep * kk, idesc, (kb | kk) != 0);
-            } else {
-              umma_bf16(d_tmem, adesc + kStep * kk, bdesc + kStep * kk, idesc, (kb | kk) != 0);
-            }
+          } else {
+            umma_bf16_e(d_tmem, adesc + kStep * kk, bdesc + kStep * kk, idesc, (kb | kk) != 0);
           }
-          if constexpr (CG == 2)
-            umma_commit_cg2(&empty[stage], CL == 4 ? 0xF : 0x3);  // frees the stage (all CTAs that wrote it)
-          else
-            umma_commit(&empty[stage]);
         }
-        __syncwarp();
+        if constexpr (CG == 2)
+          umma_commit_cg2_e(&empty[stage], CL == 4 ? 0xF : 0x3);  // frees the stage (all CTAs that wrote it)
+        else
+          umma_commit_e(&empty[stage]);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
-      if (lane == 0) {
-        if constexpr (CG == 2)
-          umma_commit_cg2(&tfull[acc], (uint16_t)(0x3u << pl));
-        else
-          umma_commit(&tfull[acc]);
-      }
-      __syncwarp();
+      if constexpr (CG == 2)
+        umma_commit_cg2_e(&tfull[acc], (uint16_t)(0x3u << pl));
+      else
+        umma_commit_e(&tfull[acc]);
       if (++acc == AS) {
         acc = 0;
         acc_phase ^= 1;

@@ -6,6 +6,8 @@
 //           completion through cp.async.mbarrier.arrive.noinc
 //   mode 2  plain LDG 16 B by 4 warps into registers (no smem), the same order
 //   mode 3  TMA 1-D bulk copies of 16 KB contiguous (4 whole rows per k-block)
+//   mode 4  mode 0 with the consumer holding every stage `hold` SM cycles before
+//           freeing it (stands in for the MMA -> commit latency of the gate)
 // One consumer warp per CTA waits each stage and frees it (modes 0, 1, 3).
 // L2 is flushed (512 MB write) before every launch; median of 20 launches.
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a
@@ -31,7 +33,7 @@ constexpr int kUnits = kRows / kUnit;         // 512
 template <int MODE, int STAGES>
 __global__ void __launch_bounds__(192, 1)
     stream_kernel(const __grid_constant__ CUtensorMap map, const __nv_bfloat16* x,
-                  unsigned long long* sink, long long* cycles) {
+                  unsigned long long* sink, long long* cycles, int hold) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[STAGES], empty[STAGES];
@@ -58,13 +60,13 @@ __global__ void __launch_bounds__(192, 1)
             v[i] = __ldg(reinterpret_cast<const uint4*>(x + (size_t)r * kCols + kb * kBK) + (lane % 8));
           }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc ^= (unsigned long long)v[i].x ^ v[i].w;
+          for (int i = 0; i < 8; ++i) acc += (unsigned long long)v[i].x + v[i].y + v[i].z + v[i].w;
         }
       }
     }
   } else if (warp == 0) {
     // producer(s)
-    if (MODE == 0 || MODE == 3) {
+    if (MODE == 0 || MODE == 3 || MODE == 4) {
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < kUnits; u += gridDim.x) {
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[stage], kStageBytes);
-            if (MODE == 0)
+            if (MODE == 0 || MODE == 4)
               tma_load_2d(smem + stage * kStageBytes, &map, &full[stage], kb * kBK, u * kUnit);
             else
               bulk_load(smem + stage * kStageBytes,
@@ -93,6 +95,11 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&full[stage], phase);
         if (lane == 0) {
           acc ^= *reinterpret_cast<volatile unsigned long long*>(smem + stage * kStageBytes + 8 * (kb & 7));
+          if (MODE == 4) {  // hold the stage (in flight, like an MMA reading it)
+            const long long t = clock64();
+            while (clock64() - t < hold) {
+            }
+          }
           mbar_arrive(&empty[stage]);
         }
         __syncwarp();
@@ -134,7 +141,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 template <int MODE, int STAGES>
 static void run(const CUtensorMap& map, const __nv_bfloat16* x, uint8_t* flush, unsigned long long* sink,
-                long long* cyc, int grid) {
+                long long* cyc, int grid, int hold = 0) {
   const int smem = STAGES * kStageBytes + 1024;
   cudaFuncSetAttribute(stream_kernel<MODE, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t e0, e1;
@@ -146,7 +153,7 @@ static void run(const CUtensorMap& map, const __nv_bfloat16* x, uint8_t* flush, 
   for (int it = 0; it < 23; ++it) {
     cudaMemsetAsync(flush, it & 0xff, 512ull << 20);
     cudaEventRecord(e0);
-    stream_kernel<MODE, STAGES><<<grid, 192, smem>>>(map, x, sink, cyc);
+    stream_kernel<MODE, STAGES><<<grid, 192, smem>>>(map, x, sink, cyc, hold);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -160,8 +167,8 @@ static void run(const CUtensorMap& map, const __nv_bfloat16* x, uint8_t* flush, 
   const float us = ts[ts.size() / 2];
   const double bytes = (double)kRows * kCols * 2;
   const double per_sm = bytes / grid;
-  printf("mode %d stages %2d grid %3d  %7.1f us  %6.0f GB/s  max CTA %6.1f kcycles  %5.1f B/clk/SM%s\n",
-         MODE, STAGES, grid, us, bytes / us / 1e3, cmax / 1e3,
+  printf("mode %d hold %5d stages %2d grid %3d  %7.1f us  %6.0f GB/s  max CTA %6.1f kcycles  %5.1f B/clk/SM%s\n",
+         MODE, hold, STAGES, grid, us, bytes / us / 1e3, cmax / 1e3,
          per_sm * ((double)((kUnits + grid - 1) / grid) / ((double)kUnits / grid)) / cmax,
          err == cudaSuccess ? "" : cudaGetErrorString(err));
 }
@@ -190,14 +197,18 @@ int main() {
   }
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  for (int grid : {sms, 128}) {
+  for (int grid : {sms}) {
     run<0, 8>(map, x, flush, sink, cyc, grid);
-    run<0, 12>(map, x, flush, sink, cyc, grid);
     run<1, 8>(map, x, flush, sink, cyc, grid);
-    run<1, 12>(map, x, flush, sink, cyc, grid);
     run<2, 8>(map, x, flush, sink, cyc, grid);
     run<3, 8>(map, x, flush, sink, cyc, grid);
-    run<3, 12>(map, x, flush, sink, cyc, grid);
+    // ring depth: an MMA that holds each stage until it completes shortens the
+    // effective ring (mode 0 with fewer stages)
+    run<0, 2>(map, x, flush, sink, cyc, grid);
+    run<0, 3>(map, x, flush, sink, cyc, grid);
+    run<0, 4>(map, x, flush, sink, cyc, grid);
+    run<0, 6>(map, x, flush, sink, cyc, grid);
+    for (int hold : {100, 200, 400}) run<4, 8>(map, x, flush, sink, cyc, grid, hold);
   }
   return 0;
 }
