@@ -556,6 +556,9 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's own messages (e.g. NCCL_DEBUG=VERSION's banner) go to stderr: rank 0's
+        # stdout carries exactly one JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     wl = WORKLOADS[args.workload]
     S = args.tokens or wl["S"]
