@@ -533,6 +533,14 @@ MOE_DEV float gelu_tanh_accurate(float x) {
   return 0.5f * x * (1.0f + tanhf(inner));
 }
 
+// 2^x on the MUFU (ex2.approx.ftz: 2 ulp); exp(v - m) = ex2(fma(v, log2e, -m*log2e))
+MOE_DEV float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kLog2e = 1.4426950408889634f;
+
 MOE_DEV float tanh_fast(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -17,6 +17,8 @@
 // The fp32 accumulator is double buffered in TMEM (2 x BN columns) so the
 // epilogue of tile i overlaps the MMAs of tile i+1.
 #include "common.cuh"
+#include <type_traits>
+
 #include "moe_kernels.h"
 
 #include <cudaTypedefs.h>
@@ -1272,31 +1274,42 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         const bool valid = local_row + ms * TM < rows_g && !g_skip;
         float b1 = -INFINITY, b2 = -INFINITY;
         int i1 = 0x7fffffff, i2 = 0x7fffffff;
+        // top-k scan; K1: the arg-max alone (k = 1: 3 instructions per logit, not 8)
+        auto topk_scan = [&](auto k1) {
+          constexpr bool K1 = decltype(k1)::value;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_addr + c * 32, r);
-          tmem_ld_wait();
-          // ascending column order + strict compare keeps the lower index on ties
-          // (branch-free selects; padded columns >= E are masked to -inf)
-          const bool full_chunk = c * 32 + 32 <= E;
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(t_addr + c * 32, r);
+            tmem_ld_wait();
+            // ascending column order + strict compare keeps the lower index on ties
+            // (branch-free selects; padded columns >= E are masked to -inf)
+            const bool full_chunk = c * 32 + 32 <= E;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int col = c * 32 + i;
-            const float v = (full_chunk || col < E) ? __uint_as_float(r[i]) : -INFINITY;
-            const bool g1 = v > b1, g2 = v > b2;
-            b2 = g1 ? b1 : (g2 ? v : b2);
-            i2 = g1 ? i1 : (g2 ? col : i2);
-            b1 = g1 ? v : b1;
-            i1 = g1 ? col : i1;
-          }
-          if (valid && args.logits != nullptr) {
-            float* lrow = args.logits + t * E;
+            for (int i = 0; i < 32; ++i) {
+              const int col = c * 32 + i;
+              const float v = (full_chunk || col < E) ? __uint_as_float(r[i]) : -INFINITY;
+              const bool g1 = v > b1;
+              if constexpr (!K1) {
+                const bool g2 = v > b2;
+                b2 = g1 ? b1 : (g2 ? v : b2);
+                i2 = g1 ? i1 : (g2 ? col : i2);
+              }
+              b1 = g1 ? v : b1;
+              i1 = g1 ? col : i1;
+            }
+            if (valid && args.logits != nullptr) {
+              float* lrow = args.logits + t * E;
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c * 32 + i < E) lrow[c * 32 + i] = __uint_as_float(r[i]);
+              for (int i = 0; i < 32; ++i)
+                if (c * 32 + i < E) lrow[c * 32 + i] = __uint_as_float(r[i]);
+            }
           }
-        }
+        };
+        if (args.k == 1)
+          topk_scan(std::true_type{});
+        else
+          topk_scan(std::false_type{});
         // Rows with fewer than k values above -inf (NaN / -inf logits, e.g. after a
         // diverged step) re-rank with np.argsort(-logits, kind="stable") semantics:
         // NaN after every number, -inf before NaN, ties to the lower index - so
@@ -1324,7 +1337,10 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           }
           if (slow) { b1 = s1; i1 = j1; b2 = s2; i2 = j2; }
         }
+        // softmax denominator: exp(v - b1) = 2^(v*log2e - b1*log2e) on the MUFU (one FFMA +
+        // one EX2 per logit; +-inf / NaN rows give the same inf / NaN / 0 terms as expf)
         float sum = 0.f;
+        const float nb1 = -b1 * kLog2e;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
@@ -1332,11 +1348,11 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           tmem_ld_wait();
           if (c * 32 + 32 <= E) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) sum += expf(__uint_as_float(r[i]) - b1);
+            for (int i = 0; i < 32; ++i) sum += ex2_approx(fmaf(__uint_as_float(r[i]), kLog2e, nb1));
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (c * 32 + i < E) sum += expf(__uint_as_float(r[i]) - b1);
+              if (c * 32 + i < E) sum += ex2_approx(fmaf(__uint_as_float(r[i]), kLog2e, nb1));
           }
         }
         if (args.probsum != nullptr) {
