@@ -556,10 +556,19 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        # NCCL's own messages (e.g. NCCL_DEBUG=VERSION's banner) go to stderr: rank 0's
-        # stdout carries exactly one JSON line
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL's own banner (NCCL_DEBUG=VERSION prints it on stdout when the first
+        # communicator comes up) goes to stderr: rank 0's stdout carries one JSON line
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=dev)
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     wl = WORKLOADS[args.workload]
     S = args.tokens or wl["S"]
     M, E, k, cf, residual = wl["M"], wl["E"], wl["k"], wl["cf"], wl["residual"]

@@ -1687,7 +1687,7 @@ template <int BN, int STAGES, int EPI, int CG = 1, int EW = 4, int CL = CG, int 
           int MS = 1>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
                      int64_t max_tiles, cudaStream_t st, const CUtensorMap* md = nullptr,
-                     int64_t grid_cap = 0, const CUtensorMap* ma2 = nullptr) {
+                     int64_t grid_cap = 0, const CUtensorMap* ma2 = nullptr, int ctas_per_sm = 1) {
   using L = Smem<BN, STAGES, CG, out_stage_bytes<EPI, EW, CG, BN>(), MS>;
   static_assert(L::kTotal <= 227 * 1024, "dynamic shared memory beyond the 227 KB per CTA");
   auto kern = gemm_bf16_tc_kernel<BN, STAGES, EPI, CG, EW, CL, SUB, MS>;
@@ -1696,7 +1696,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
     cudaError_t e = ensure_smem_attr(kern, L::kTotal, attr_done);
     if (e != cudaSuccess) return (int)e;
   }
-  int64_t grid = num_sms();
+  int64_t grid = (int64_t)num_sms() * ctas_per_sm;
   if (gemm_cta_limit() > 0 && gemm_cta_limit() < grid) grid = gemm_cta_limit();
   if (grid_cap > 0 && grid_cap < grid) grid = grid_cap;
   // max_tiles counts cluster tiles (CL/CG pairs each)
@@ -2252,6 +2252,16 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
     return launch_tc<128, 5, EPI_GATE, 2, 4, 2, 1, 2>(ma, mb, a, tiles2, st);
   }
   const int64_t tiles = (S + (int64_t)BM * CG * CLP - 1) / ((int64_t)BM * CG * CLP);
+  // MOE_GATE_2CTA (default 1; E in (64, 128], pairs): two gate CTAs per SM, each with a
+  // 4-stage ring - twice the producer / MMA issue streams per SM. Behind the power-capped
+  // GEMM2 (~1 GHz) the gate is issue-bound, not HBM-bound: 80 -> 69 us at base clock,
+  // 54 -> 52 us unlocked (profiles/r2_gate_2cta.log)
+  static const int gate_2cta = [] {
+    const char* v = getenv("MOE_GATE_2CTA");
+    return v ? atoi(v) : 1;
+  }();
+  if (gate_2cta == 1 && CG == 2 && CLP == 1 && BN == 128 && !a.gate_bal)
+    return launch_tc<128, 4, EPI_GATE, 2, 4>(ma, mb, a, tiles, st, nullptr, 0, nullptr, 2);
   if (CLP == 2)
     return BN == 128 ? launch_tc<128, 8, EPI_GATE, 2, 4, 4>(ma, mb, a, tiles, st)
                      : launch_tc<256, 6, EPI_GATE, 2, 4, 4>(ma, mb, a, tiles, st);

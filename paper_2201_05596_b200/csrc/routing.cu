@@ -176,9 +176,22 @@ __global__ void plan_scan_kernel(const int32_t* __restrict__ tile_counts, int64_
   const int e = blockIdx.x * 32 + tx;
   const int64_t chunk = (T + 31) / 32;
   const int64_t lo = ty * chunk, hi = min(T, lo + chunk);
+  // chunk <= kReg (T <= 512 routing tiles = 65,536 tokens): the column's counts are
+  // loaded once, all at the same time, and kept in registers for the second pass
+  constexpr int kReg = 16;
+  int v[kReg];
+  const bool in_regs = chunk <= kReg;
   int s = 0;
-  if (e < E)
-    for (int64_t i = lo; i < hi; ++i) s += tile_counts[i * E + e];
+  if (e < E) {
+    if (in_regs) {
+#pragma unroll
+      for (int j = 0; j < kReg; ++j) v[j] = lo + j < hi ? tile_counts[(lo + j) * E + e] : 0;
+#pragma unroll
+      for (int j = 0; j < kReg; ++j) s += v[j];
+    } else {
+      for (int64_t i = lo; i < hi; ++i) s += tile_counts[i * E + e];
+    }
+  }
   part[ty][tx] = s;
   __syncthreads();
   if (ty == 0) {
@@ -200,9 +213,17 @@ __global__ void plan_scan_kernel(const int32_t* __restrict__ tile_counts, int64_
   __syncthreads();
   if (e < E) {
     int run = part[ty][tx];
-    for (int64_t i = lo; i < hi; ++i) {
-      tile_offsets[i * E + e] = run;
-      run += tile_counts[i * E + e];
+    if (in_regs) {
+#pragma unroll
+      for (int j = 0; j < kReg; ++j) {
+        if (lo + j < hi) tile_offsets[(lo + j) * E + e] = run;
+        run += v[j];
+      }
+    } else {
+      for (int64_t i = lo; i < hi; ++i) {
+        tile_offsets[i * E + e] = run;
+        run += tile_counts[i * E + e];
+      }
     }
   }
 }
