@@ -3,5 +3,5 @@ M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_secto
 for w in c3 c2 c4-32 c4-64; do python tools/profile_step.py --workload $w > gpurun_out/plain_$w.log 2>&1; done
 for w in c3 c4-32 c4-64; do ncu --metrics $M --clock-control none -k regex:"gemm_bf16|scatter|plan_scan|combine" -s 15 -c 5 --csv --log-file gpurun_out/r2_launches_$w.csv python tools/profile_step.py --workload $w > /dev/null 2>&1; done
 ncu --metrics $M --clock-control none -k regex:"gemm_bf16|scatter|plan_scan|combine" -s 18 -c 6 --csv --log-file gpurun_out/r2_launches_c2.csv python tools/profile_step.py --workload c2 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"gemm_bf16_tc_kernel<128, 8, 2|scatter_kernel" -s 6 -c 2 -o gpurun_out/r2_gate_dispatch python tools/profile_step.py --workload c3 > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"gemm_bf16_tc_kernel|scatter_kernel" -s 8 -c 2 -o gpurun_out/r2_gate_dispatch python tools/profile_step.py --workload c3 > gpurun_out/ncu_full.log 2>&1
 echo done
