@@ -14,8 +14,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c3")
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--tokens", type=int, default=None, help="tokens (default: the workload's)")
 a = ap.parse_args()
-wl = bench.WORKLOADS[a.workload]
+wl = dict(bench.WORKLOADS[a.workload])
+if a.tokens:
+    wl["S"] = a.tokens
 dev = torch.device("cuda", 0)
 layer = bench.make_layer(wl["S"], wl["M"], wl["E"], wl["k"], wl["cf"], dev, residual=wl["residual"])
 x = torch.randn(wl["S"], wl["M"], device=dev, generator=torch.Generator(device=dev).manual_seed(1)
