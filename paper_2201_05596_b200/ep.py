@@ -311,6 +311,7 @@ class EPMoeLayer:
         if S:
             _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k, None,
                       ids.data_ptr(), gp.data_ptr(), lr.data_ptr(), tc.data_ptr(), st)
+        ph("scan")
         # local per-expert counts (cap irrelevant here)
         _lib.call("moe_plan_scan", tc.data_ptr(), S, E, 2 ** 62, None,
                   ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
@@ -525,6 +526,7 @@ class EPMoeLayer:
         if S:
             _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k, None,
                       ids.data_ptr(), gp.data_ptr(), lr.data_ptr(), tc.data_ptr(), stream)
+        ph("scan")
         _lib.call("moe_plan_scan", tc.data_ptr(), S, E, 2 ** 62, None,
                   ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
                   stream)
@@ -845,6 +847,7 @@ class SlicedEPMoeLayer(EPMoeLayer):
         if S:
             _lib.call("moe_gate_gemm_bf16", x.data_ptr(), self.wg.data_ptr(), S, M, E, k, None,
                       ids.data_ptr(), gp.data_ptr(), lr.data_ptr(), tc.data_ptr(), st)
+        ph("scan")
         _lib.call("moe_plan_scan", tc.data_ptr(), S, E, 2 ** 62, None,
                   ws["tile_offsets"].data_ptr(), ws["totals"].data_ptr(), ws["kept"].data_ptr(),
                   st)
