@@ -123,7 +123,6 @@ struct GemmArgs {
   int64_t c_cap;
   int64_t c_tokens;           // S
   int* c_done;                // zeroed: expert-tile epilogue warps done storing y
-  int c_nowait;               // timing experiment only (MOE_RESID_NOWAIT=1): skip the wait
   const int32_t* c_row_index; // [S, k] row of y per choice (-1 dropped), or null: e*cap+slot
   // EP push return (EPI_BIAS / EPI_BIAS_COMBINE): valid row r is stored to rank
   // row_src[r]'s buffer push_base[row_src[r]] at row row_token[r] (over NVLink)
@@ -879,7 +878,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             // every expert tile's y must be stored first: the expert tiles precede the
             // shared ones in tile order and every CTA runs its tiles in order, so they
             // are all claimed by running CTAs and complete without waiting on this one
-            const int expected = args.c_nowait ? 0 : tile_start[args.rc_group] * EW * CG;
+            const int expected = tile_start[args.rc_group] * EW * CG;
             if (lane == 0) {
               while (ld_acquire_gpu(args.c_done) < expected) __nanosleep(256);
             }
@@ -2127,11 +2126,6 @@ int launch_residual_gemm_bf16(const void* A, int64_t a_rows, const void* A2, int
   a.out = (__nv_bfloat16*)out;
   // the completion counter: a zeroed slot of the per-device pool (graph-safe)
   a.c_done = dyn_counter(st, 0, 0, true);
-  static const int nowait = [] {
-    const char* v = getenv("MOE_RESID_NOWAIT");
-    return v ? atoi(v) : 0;
-  }();
-  a.c_nowait = nowait;
   if (a.c_done == nullptr) return MOE_EINVAL;
   a.tile_counter = dyn_counter(st, K, N);
   if (CG == 2) {
