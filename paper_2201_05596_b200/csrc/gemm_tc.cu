@@ -46,6 +46,24 @@ namespace moe {
 //     outputs y); groups >= rc_group are the shared MLP, whose epilogue waits until
 //     every expert tile has stored (device counter) and emits
 //     out[t] = (x[t] + sum_j p_j y[e_j*cap + slot_j]) + (acc + b2_shared).
+// MOE_GATE_TRACE (debug builds only, tools/gate_trace.sh): %globaltimer stamps of
+// the gate's phases in CTA 0, read back with moe_debug_gate_trace()
+#ifdef MOE_GATE_TRACE
+__device__ unsigned long long g_gate_trace[16];
+#define GATE_TRACE(i)                                                              \
+  do {                                                                             \
+    if (EPI == EPI_GATE && blockIdx.x == 0) {                                      \
+      unsigned long long t_;                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                       \
+      g_gate_trace[i] = t_;                                                        \
+    }                                                                              \
+  } while (0)
+#else
+#define GATE_TRACE(i) \
+  do {                \
+  } while (0)
+#endif
+
 enum { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_GATE = 2, EPI_BIAS_COMBINE = 3, EPI_GELU_SAVE = 4,
        EPI_GELU_BWD = 5, EPI_WGRAD = 6, EPI_WGRAD_ACC = 7, EPI_BIAS_RESID = 8,
        EPI_COMBINE_PUSH = 9 };
@@ -230,6 +248,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   constexpr int kPW = BN / kParts;
   constexpr bool kMN = EPI == EPI_WGRAD || EPI == EPI_WGRAD_ACC;  // MN-major operands
   extern __shared__ uint8_t smem_raw[];
+  if (threadIdx.x == 0) GATE_TRACE(0);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -324,6 +343,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
   tc_fence_after();
   pdl_wait();  // every role: no global access before the predecessor grid completed
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) GATE_TRACE(1);
   const int total_tiles = tile_start[G];
 
   // Work order: tiles are numbered (group, m block, n block) with n fastest and
@@ -454,7 +474,8 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       if (EPI == EPI_GATE && args.prefetch_cur && lane == 0) {
         // one tile per CTA (decode-sized batches): the K blocks the ring cannot hold
         // yet are requested into L2 at once, so the ring refills from L2 instead of
-        // paying a DRAM round trip per stage (W_g^T rows and this CTA's x rows)
+        // paying a DRAM round trip per stage (W_g^T rows and this CTA's x rows;
+        // issuing them after the ring's first loads measured 1.2 us slower)
         for (int kb = STAGES; kb < num_kb; ++kb) {
           tma_prefetch_l2_2d(mA, kb * BK, a_row);
           tma_prefetch_l2_2d(&map_b, kb * BK, b_row);
@@ -497,6 +518,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       }
       for (int kb = 0; kb < kb_end; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0 && vit == 0 && kb == 0) GATE_TRACE(2);
         if constexpr (kMN) {
           // X^T / Y^T tiles: boxes of 64 MN columns x 64 token rows (one 128-B
           // line per row); A = this CTA's BM columns of X, B = its BN/CG of Y
@@ -733,6 +755,8 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       for (int kb = 0; kb < kb_end; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (lane == 0 && vit == 0 && kb == 0) GATE_TRACE(3);
+        if (lane == 0 && vit == 0 && kb == kb_end - 1) GATE_TRACE(4);
         const uint8_t* sa = smem + stage * L::kStageBytes;
         const uint8_t* sb = sa + L::kABytes;
         const uint64_t adesc = kMN ? make_sdesc_sw128_mn(sa) : make_sdesc_sw128(sa);
@@ -814,6 +838,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       if constexpr (kMN) kzero = (args.k_rows ? args.k_rows[g] : args.k_rows_const) == 0;
 
       mbar_wait(&tfull[kSplit ? 0 : acc], acc_phase);
+      if (warp == 2 && lane == 0 && vit == 0) GATE_TRACE(5);
       tc_fence_after();
       // TMEM column and tile column of this warp's 32-column chunk c. kSplit: chunks
       // 2j, 2j+1 lie in column part j (handed over separately); part j's first
@@ -1283,7 +1308,12 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
         const bool valid = local_row + ms * TM < rows_g && !g_skip;
         float b1 = -INFINITY, b2 = -INFINITY;
         int i1 = 0x7fffffff, i2 = 0x7fffffff;
-        // top-k scan; K1: the arg-max alone (k = 1: 3 instructions per logit, not 8)
+        // top-k scan; K1: the arg-max alone (k = 1: 3 instructions per logit, not 8), as
+        // four interleaved chains (columns i mod 4, each ascending with a strict compare,
+        // merged below preferring the lower index on equal values) so the dependent
+        // select chain is a quarter as long
+        float pb[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        int pi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
         auto topk_scan = [&](auto k1) {
           constexpr bool K1 = decltype(k1)::value;
 #pragma unroll 1
@@ -1298,14 +1328,17 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             for (int i = 0; i < 32; ++i) {
               const int col = c * 32 + i;
               const float v = (full_chunk || col < E) ? __uint_as_float(r[i]) : -INFINITY;
-              const bool g1 = v > b1;
-              if constexpr (!K1) {
-                const bool g2 = v > b2;
+              if constexpr (K1) {
+                const bool g = v > pb[i & 3];
+                pb[i & 3] = g ? v : pb[i & 3];
+                pi[i & 3] = g ? col : pi[i & 3];
+              } else {
+                const bool g1 = v > b1, g2 = v > b2;
                 b2 = g1 ? b1 : (g2 ? v : b2);
                 i2 = g1 ? i1 : (g2 ? col : i2);
+                b1 = g1 ? v : b1;
+                i1 = g1 ? col : i1;
               }
-              b1 = g1 ? v : b1;
-              i1 = g1 ? col : i1;
             }
             if (valid && args.logits != nullptr) {
               float* lrow = args.logits + t * E;
@@ -1315,10 +1348,18 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             }
           }
         };
-        if (args.k == 1)
+        if (args.k == 1) {
           topk_scan(std::true_type{});
-        else
+          if (warp == 2 && lane == 0 && vit == 0) GATE_TRACE(9);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {  // merge: larger value, then lower index
+            const bool g = pb[j] > b1 || (pb[j] == b1 && pi[j] < i1);
+            b1 = g ? pb[j] : b1;
+            i1 = g ? pi[j] : i1;
+          }
+        } else {
           topk_scan(std::false_type{});
+        }
         // Rows with fewer than k values above -inf (NaN / -inf logits, e.g. after a
         // diverged step) re-rank with np.argsort(-logits, kind="stable") semantics:
         // NaN after every number, -inf before NaN, ties to the lower index - so
@@ -1356,14 +1397,17 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           tmem_ld_32x32b_x32(t_addr + c * 32, r);
           tmem_ld_wait();
           if (c * 32 + 32 <= E) {
+            float ps[4] = {0.f, 0.f, 0.f, 0.f};  // four partial sums: a quarter-length FADD chain
 #pragma unroll
-            for (int i = 0; i < 32; ++i) sum += ex2_approx(fmaf(__uint_as_float(r[i]), kLog2e, nb1));
+            for (int i = 0; i < 32; ++i) ps[i & 3] += ex2_approx(fmaf(__uint_as_float(r[i]), kLog2e, nb1));
+            sum += (ps[0] + ps[1]) + (ps[2] + ps[3]);
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               if (c * 32 + i < E) sum += ex2_approx(fmaf(__uint_as_float(r[i]), kLog2e, nb1));
           }
         }
+        if (warp == 2 && lane == 0 && vit == 0) GATE_TRACE(10);
         if (args.probsum != nullptr) {
           // load-balance statistics (arch.py:297-313): column sums of the full softmax,
           // reduced across the warp with a transpose-reduce (lane l ends with column l)
@@ -1412,6 +1456,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             args.gate_probs[t * k + 1] = expf(b2 - b1) / sum;
           }
         }
+        if (warp == 2 && lane == 0 && vit == 0) GATE_TRACE(11);
         // per-tile capacity ranks (token-major order, gating.py:226)
         // 4 x E per-warp counters in the tile-table region (G == 1 uses [0, 2))
         int* wc = reinterpret_cast<int*>(smem + L::kTileOff) + 8;
@@ -1445,6 +1490,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           args.local_rank[t * k] = r0;
           if (k == 2) args.local_rank[t * k + 1] = r1;
         }
+        if (warp == 2 && lane == 0 && vit == 0) GATE_TRACE(12);
         const int64_t tile_row0 = gbal ? (int64_t)tile * BM + cta * BM
                                        : (int64_t)mb * TMC + pair * TM + ms * TM + cta * BM;  // this CTA's routing tile
         if (tile_row0 < args.S && !g_skip)
@@ -1453,6 +1499,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
                 wc[e] + wc[E + e] + wc[2 * E + e] + wc[3 * E + e];
         named_bar_sync(1, 128);
         }  // ms
+        if (warp == 2 && lane == 0 && vit == 0) GATE_TRACE(6);
       }
       if (++acc == AS) {
         acc = 0;
@@ -1520,6 +1567,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     }
   }
 
+  if (threadIdx.x == 0) GATE_TRACE(7);
   tc_fence_before();
   if constexpr (CG == 2)
     cluster_sync();  // the peer's TMEM is written by the leader's MMAs: free only when both done
@@ -1532,6 +1580,7 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
     else
       tmem_dealloc(tmem_base, tmem_cols<BN, MS>());
   }
+  if (threadIdx.x == 0) GATE_TRACE(8);
 }
 
 // ============================================================ host side
@@ -2285,3 +2334,9 @@ int launch_gate_gemm_bf16(const void* x, const void* wg_t, int64_t S, int M, int
 }
 
 }  // namespace moe
+
+#ifdef MOE_GATE_TRACE
+extern "C" int moe_debug_gate_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, moe::g_gate_trace, sizeof(unsigned long long) * 16);
+}
+#endif
