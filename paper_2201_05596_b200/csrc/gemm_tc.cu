@@ -471,16 +471,6 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
           grow[i] = lr < rg ? args.a_gather[rs + lr] : 0;
         }
       }
-      if (EPI == EPI_GATE && args.prefetch_cur && lane == 0) {
-        // one tile per CTA (decode-sized batches): the K blocks the ring cannot hold
-        // yet are requested into L2 at once, so the ring refills from L2 instead of
-        // paying a DRAM round trip per stage (W_g^T rows and this CTA's x rows;
-        // issuing them after the ring's first loads measured 1.2 us slower)
-        for (int kb = STAGES; kb < num_kb; ++kb) {
-          tma_prefetch_l2_2d(mA, kb * BK, a_row);
-          tma_prefetch_l2_2d(&map_b, kb * BK, b_row);
-        }
-      }
       if (args.prefetch && !dyn && gbal && lane == 0) {
         // balanced gate: the next routing-tile pair of this pair's range (an odd last
         // routing tile is the leader's alone)
@@ -836,6 +826,21 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
       const int64_t out_row = rs + local_row;
       bool kzero = false;  // weight gradient of a group with no rows: zeros, TMEM not written
       if constexpr (kMN) kzero = (args.k_rows ? args.k_rows[g] : args.k_rows_const) == 0;
+      if constexpr (EPI == EPI_GATE) {
+        if (args.prefetch_cur && warp == 2 && lane == 0) {
+          // one tile per CTA (decode-sized batches): while the producer issues the
+          // ring's first loads, this (still idle) warp requests the K blocks the ring
+          // cannot hold yet into L2, so the ring refills from L2 instead of paying a
+          // DRAM round trip per stage (this CTA's x rows and its W_g^T rows)
+          const int a_row = (int)(rs + (int64_t)mb * TMC + sub * TM + pair * TM + cta * BM);
+          const int b_row = w * args.N + nb * BN + cta * (BN / CG);
+          const int num_kb = (args.K + BK - 1) / BK;
+          for (int kb = STAGES; kb < num_kb; ++kb) {
+            tma_prefetch_l2_2d(&map_a, kb * BK, a_row);
+            tma_prefetch_l2_2d(&map_b, kb * BK, b_row);
+          }
+        }
+      }
 
       mbar_wait(&tfull[kSplit ? 0 : acc], acc_phase);
       if (warp == 2 && lane == 0 && vit == 0) GATE_TRACE(5);
