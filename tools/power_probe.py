@@ -128,6 +128,7 @@ SETS = {
             ("grouped_gemm2_fused_combine", g2c), ("grouped_gemm2_tma", g2t),
             ("cublas_bmm2_per_expert_w", bb2)) * 2,
 }
+SETS["g2c"] = (("grouped_gemm2_fused_combine", g2c), ("grouped_gemm2_tma", g2t)) * 2
 SETS["none"] = ()  # (operands only: tools/burst_vs_cublas.py imports this module)
 for name, fn in SETS[os.environ.get("PROBE_SET", "all")]:
     probe(name, fn)
