@@ -467,3 +467,18 @@ if torch.cuda.device_count() >= 2:  # collected on multi-GPU boxes only
             torch.cuda.synchronize(0)
             torch.cuda.synchronize(1)
             assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+@pytest.mark.parametrize("S,k", [(20500, 1), (20500, 2), (38011, 1), (37, 1), (200, 2)])
+def test_gate_launch_configurations_routing(S, k):
+    """The fused gate's launch shapes at E=128: two CTAs per SM once the pair tiles
+    exceed one per SM pair (S > 74 x 256; ragged last routing tile), and the
+    single-wave launch whose idle epilogue warp L2-prefetches the tile (decode
+    sizes). Routing bit-exact, slots / loads exact, probabilities to 2e-6."""
+    M, E = 512, 128
+    spec = A.LayerSpec(kind="moe", hidden=M, experts=E, gating=GatingConfig(E, k, 1.25))
+    p = rounded_params(spec, 4242 + S + k, torch.bfloat16)
+    gen = torch.Generator().manual_seed(S + 7 * k)
+    x64 = torch.randn(S, M, generator=gen).to(torch.bfloat16).double().numpy()
+    layer, x, out, logits = run_layer(spec, p, x64, torch.bfloat16)
+    check_routing(layer, logits, spec, S)
