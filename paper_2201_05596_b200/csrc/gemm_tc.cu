@@ -1329,20 +1329,32 @@ __global__ void __launch_bounds__(threads_for<EW, EPI>(), 1)
             // ascending column order + strict compare keeps the lower index on ties
             // (branch-free selects; padded columns >= E are masked to -inf)
             const bool full_chunk = c * 32 + 32 <= E;
+            // K1: chunk-local chains whose index is the compile-time column in the
+            // chunk (a select of an immediate), folded into pb / pi after the chunk
+            float qb[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            int qi[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int col = c * 32 + i;
               const float v = (full_chunk || col < E) ? __uint_as_float(r[i]) : -INFINITY;
               if constexpr (K1) {
-                const bool g = v > pb[i & 3];
-                pb[i & 3] = g ? v : pb[i & 3];
-                pi[i & 3] = g ? col : pi[i & 3];
+                const bool g = v > qb[i & 3];
+                qb[i & 3] = g ? v : qb[i & 3];
+                qi[i & 3] = g ? i : qi[i & 3];
               } else {
                 const bool g1 = v > b1, g2 = v > b2;
                 b2 = g1 ? b1 : (g2 ? v : b2);
                 i2 = g1 ? i1 : (g2 ? col : i2);
                 b1 = g1 ? v : b1;
                 i1 = g1 ? col : i1;
+              }
+            }
+            if constexpr (K1) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {  // later chunks hold higher columns: strict >
+                const bool g = qb[j] > pb[j];
+                pb[j] = g ? qb[j] : pb[j];
+                pi[j] = g ? c * 32 + qi[j] : pi[j];
               }
             }
             if (valid && args.logits != nullptr) {
